@@ -1,0 +1,371 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(SURVEY.md §8(c) P1-P14).  No GPU, no CUDA library: these run with -m "not gpu".
+
+Each test names the pin and the passage it follows.  None of them re-types the
+oracle's own formula; they check worked examples, closed forms, invariants,
+brute force and a third exact-rational implementation (tests/exact_rational.py).
+"""
+
+from __future__ import annotations
+
+import itertools
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_03788_b200 import synth
+from tests import exact_rational as ex
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "eq1_worked_examples.json")
+
+
+def _golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def _bits(x: float) -> int:
+    return int(np.float16(x).view(np.uint16))
+
+
+# ---------------------------------------------------------------- P1-P4
+@pytest.mark.parametrize("case", _golden()["cases"], ids=lambda c: c["name"])
+def test_p1_p4_eq1_worked_examples(case):
+    """P1-P4: Eq. 1 worked examples."""
+    vals = np.array(case["values"], dtype=np.float16).astype(np.float64)
+    codes, delta, Z = oracle.quantize_group(vals)
+    assert codes == case["codes"]
+    assert _bits(delta) == int(case["delta_bits"], 16)
+    assert Z == case["Z"]
+    if "dequant" in case:
+        deq = [(c - Z) * delta for c in codes]
+        assert deq == case["dequant"]
+
+
+# ---------------------------------------------------------------- P5
+def test_p5_packing_example_and_exhaustive():
+    """P5: nibble packing."""
+    g = _golden()["packing"]
+    assert oracle.pack_nibbles(np.array(g["codes"])).tolist() == g["bytes"]
+    pairs = np.array(list(itertools.product(range(16), repeat=2)))
+    packed = oracle.pack_nibbles(pairs.reshape(-1))
+    assert packed.size == 256 and len(set(packed.tolist())) == 256
+    assert (oracle.unpack_nibbles(packed) == pairs.reshape(-1)).all()
+    # element 2i is the LOW nibble: a lone code at an even position stays < 16
+    assert oracle.pack_nibbles(np.array([7, 0])).tolist() == [0x07]
+    assert oracle.pack_nibbles(np.array([0, 7])).tolist() == [0x70]
+    with pytest.raises(ValueError):
+        oracle.pack_nibbles(np.array([16, 0]))
+
+
+# ---------------------------------------------------------------- P6
+@pytest.mark.parametrize("case", _golden()["eq6"]["cases"])
+def test_p6_eq6_values(case):
+    """P6: Eq. 6 values and endpoints."""
+    s = oracle.smooth_scales(np.array([case["w_max"]]), np.array([case["act_max"]], np.float32),
+                             case["alpha"])
+    assert s.dtype == np.float32
+    assert float(s[0]) == case["s"]
+
+
+def test_p6_eq6_general_alpha_closed_form():
+    """Eq. 6 for general α against the independent form exp(α ln a - (1-α) ln w)
+    (2 ulp of fp32), and the α=1 / α=0 endpoints of PAPER.md:160."""
+    g = synth.rng(3)
+    a = np.float32(g.uniform(1e-3, 2e3, size=2000)).astype(np.float32)
+    w = g.uniform(1e-3, 2.5, size=2000)
+    for alpha in (0.05, 0.35, 0.8, 0.95):
+        s = oracle.smooth_scales(w, a, alpha).astype(np.float64)
+        ref = np.exp(alpha * np.log(a.astype(np.float64)) - (1 - alpha) * np.log(w))
+        ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+        assert (np.abs(s - ref) <= 2 * ulp).all()
+    assert (oracle.smooth_scales(w, a, 1.0) == a).all()
+    assert (oracle.smooth_scales(w, a, 0.0) == (1.0 / w).astype(np.float32)).all()
+    # α = 1: every smoothed activation channel has maximum 1 (PAPER.md:160
+    # "all activation channels have the same maximum value of 1")
+    s1 = oracle.smooth_scales(w, a, 1.0).astype(np.float64)
+    assert np.allclose(a / s1, 1.0, rtol=0, atol=0)
+
+
+def test_eq6_eps_floor():
+    """Reading S10: dead channels are floored at ε = 1e-5 on both maxima."""
+    s = oracle.smooth_scales(np.array([0.0, 1.0]), np.array([1.0, 0.0], np.float32), 0.5)
+    assert float(s[0]) == np.float32(math.sqrt(1.0) / math.sqrt(1e-5))
+    assert float(s[1]) == np.float32(math.sqrt(1e-5) / math.sqrt(1.0))
+
+
+def test_absmax_brute_force():
+    """O2 / calibration statistic: per-channel max |.| by explicit loops."""
+    W = synth.weights(7, 256, seed=1)
+    wm = oracle.weight_absmax(W)
+    for k in range(256):
+        assert wm[k] == max(abs(float(W[n, k])) for n in range(7))
+    X = synth.activations(9, 64, seed=2)
+    am = oracle.act_absmax(X.astype(np.float16))
+    for k in range(64):
+        assert am[k] == np.float32(max(abs(float(np.float16(X[t, k]))) for t in range(9)))
+
+
+# ---------------------------------------------------------------- P7
+@pytest.mark.parametrize("N,K", [(48, 64), (64, 64)])
+def test_p7_eq5_equivalence(N, K):
+    """P7: Y = (X diag(s)^-1)(diag(s) W) with the oracle's fold
+    axis.  N == K catches a fold along the wrong (output) axis."""
+    g = synth.rng(11)
+    X = g.normal(size=(5, K))
+    W = synth.weights(N, K, seed=4)
+    s = np.float32(np.exp(g.uniform(np.log(1e-3), np.log(1e3), size=K))).astype(np.float32)
+    lhs = X @ W.astype(np.float64).T
+    rhs = (X / s.astype(np.float64)) @ oracle.smooth_weight_exact(W, s).T
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(lhs)
+
+
+def test_fold_is_single_rounding_of_exact_product():
+    """Reading S13: W' = RN16(w·s) computed from the exact rational product."""
+    g = synth.rng(5)
+    W = synth.weights(4, 128, seed=9, heavy=True)
+    s = g.uniform(0.01, 50.0, size=128).astype(np.float32)
+    Wf = oracle.fold(W, s)
+    for n in range(4):
+        for k in range(0, 128, 3):
+            exact = Fraction(float(W[n, k])) * Fraction(float(s[k]))
+            r = ex.rn_f16(exact)
+            assert r is not None and Fraction(Wf[n, k]) == r
+
+
+def test_rz_fp16_against_exact():
+    g = synth.rng(6)
+    xs = np.concatenate([g.uniform(0, 1, 500) * 10.0 ** g.integers(-9, 5, 500),
+                         [2.0 ** -25, 2.0 ** -24, 65504.0, 65519.0, 1e-9]])
+    h = oracle.rz_fp16(xs)
+    for x, y in zip(xs, h):
+        assert Fraction(float(y)) == ex.rz_f16(Fraction(float(x)))
+
+
+def test_rha_ties():
+    assert oracle.rha(np.array([0.5, 1.5, 2.5, -0.5, -2.5, 0.49999999999999994, -0.0])).tolist() == \
+        [1.0, 2.0, 3.0, -1.0, -3.0, 0.0, 0.0]
+
+
+# ---------------------------------------------------------------- P8-P10
+def _groups_for_invariants():
+    g = synth.rng(21)
+    gauss = synth.weights(2000, 128, seed=22).astype(np.float64)
+    edge = synth.edge_groups(128, seed=23).astype(np.float64)
+    return np.concatenate([gauss, edge])
+
+
+def _straddles_or_constant(v):
+    return (v.min() <= 0 <= v.max()) or (v.min() == v.max())
+
+
+def test_p8_idempotence():
+    """P8: Q(D(Q(W))) == Q(W) with D exact (BASELINE.json north_star
+    'quantize->dequantize idempotence'), for zero-straddling / constant groups."""
+    V = _groups_for_invariants()
+    for v in V:
+        if not _straddles_or_constant(v):
+            continue
+        c1, d1, z1 = oracle.quantize_group(v)
+        # D is exact in fp64 ((c-Z)·Δ has <= 15 significant bits); re-quantize
+        # those exact values (an fp16-rounded D is not idempotent)
+        deq = np.array([(c - z1) * d1 for c in c1])
+        c2, d2, z2 = oracle.quantize_group(deq)
+        assert (c1, _bits(d1), z1) == (c2, _bits(d2), z2)
+
+
+def test_p9_ranges():
+    """P9: codes and Z in [0, 15]; Δ > 0 finite (PAPER.md:89 clamp to [0, 2^N-1])."""
+    V = _groups_for_invariants()
+    for v in V:
+        c, d, z = oracle.quantize_group(v)
+        assert all(0 <= x <= 15 for x in c) and 0 <= z <= 15
+        assert d > 0 and math.isfinite(d)
+
+
+def test_p10_brute_force_min_error():
+    """P10: each element's reconstruction is the nearest grid point (ties allowed),
+    and zero-straddling groups obey |v - Ŵ| <= Δ/2 + max(0, r - 15Δ)."""
+    V = _groups_for_invariants()
+    for v in V:
+        c, d, z = oracle.quantize_group(v)
+        grid = np.array([(k - z) * d for k in range(16)])
+        rec = np.array([(k - z) * d for k in c])
+        err = np.abs(v - rec)
+        best = np.abs(v[:, None] - grid[None, :]).min(axis=1)
+        assert (err <= best).all()
+        if v.min() < 0 < v.max():
+            r = v.max() - v.min()
+            assert (err <= d / 2 + max(0.0, r - 15 * d)).all()
+
+
+# ---------------------------------------------------------------- P11
+def test_p11_exact_rational_tiny_groups():
+    """P11: the fp64 oracle equals an exact Fraction quantizer on tiny groups
+    (random fp16 bit patterns, near ties, subnormals, ±65504)."""
+    g = synth.rng(31)
+    cases = []
+    for size in (1, 2, 3, 4, 8):
+        for _ in range(300):
+            bits = g.integers(0, 0x7C00, size=size).astype(np.uint16)
+            bits |= (g.integers(0, 2, size=size).astype(np.uint16) << 15)
+            cases.append(bits.view(np.float16).astype(np.float64))
+    for _ in range(300):  # constructed near-ties: v = (k + 1/2)·Δ rounded to fp16
+        d = float(np.float16(g.uniform(1e-4, 1.0)))
+        k = g.integers(-8, 8, size=4)
+        v = ((k + 0.5) * d).astype(np.float16).astype(np.float64)
+        cases.append(np.concatenate([v, [-7.5 * d, 7.5 * d]]).astype(np.float16).astype(np.float64))
+    for _ in range(100):  # subnormal ranges
+        cases.append((g.integers(-1023, 1024, size=4) * 2.0 ** -24))
+    cases.append(np.array([-65504.0, 65504.0]))
+    cases.append(np.array([65504.0, 65504.0, 1.0]))
+    for v in cases:
+        c1, d1, z1 = oracle.quantize_group(v)
+        c2, d2, z2 = ex.quantize_group([float(x) for x in v])
+        assert c1 == c2 and z1 == z2 and Fraction(d1) == d2, v
+
+
+# ---------------------------------------------------------------- P12
+def test_p12_footprint():
+    """P12: fp16 Δ + fp16 Z at g=128 -> 0.265625 of fp16 bytes (PAPER.md:74 ~75% saved)."""
+    f = _golden()["footprint"]
+    assert oracle.footprint_ratio(f["N"], f["K"], f["group"]) == f["ratio"]
+    # and the layout really has that many bytes
+    q = oracle.quantize_pack(synth.weights(16, 256, seed=1), None, 128)
+    nbytes = q["Wq"].nbytes + q["scales"].nbytes + q["zeros"].nbytes
+    assert nbytes / (16 * 256 * 2) == f["ratio"]
+
+
+# ---------------------------------------------------------------- P13
+def test_p13_gemm_special_cases_and_brute_force():
+    """P13 + Eq. 2/3 orientation: Y[m][n] = sum_k X[m][k] Ŵ[n][k]
+    (PAPER.md:95-106), checked with explicit loops."""
+    N, K = 24, 256
+    W = synth.weights(N, K, seed=41)
+    q = oracle.quantize_pack(W, None, 128)
+    What = oracle.dequant(q["Wq"], q["scales"], q["zeros"], 128)
+    # dequant brute force from the stored bits
+    codes = oracle.unpack_nibbles(q["Wq"])
+    for n in range(0, N, 5):
+        for k in range(0, K, 7):
+            gi = k // 128
+            d = float(np.uint16(q["scales"][gi, n]).view(np.float16))
+            z = float(np.uint16(q["zeros"][gi, n]).view(np.float16))
+            assert What[n, k] == (codes[n, k] - z) * d
+    # identity: Y = Ŵ^T
+    Xi = np.eye(K, dtype=np.float16)
+    assert (oracle.gemm(Xi, q["Wq"], q["scales"], q["zeros"]) == What.T).all()
+    # zero
+    assert (oracle.gemm(np.zeros((3, K), np.float16), q["Wq"], q["scales"], q["zeros"]) == 0).all()
+    # brute force
+    X = synth.activations(3, K, seed=42).astype(np.float16)
+    Y = oracle.gemm(X, q["Wq"], q["scales"], q["zeros"])
+    for m in range(3):
+        for n in range(0, N, 3):
+            acc = math.fsum(float(X[m, k]) * What[n, k] for k in range(K))
+            assert abs(Y[m, n] - acc) <= 1e-12 * max(1.0, abs(acc))
+
+
+def test_quantize_pack_matches_groupwise_loop():
+    """quantize_pack == quantize_group applied per (n, group of 128 consecutive k)
+    (reading S6), including the smoothing fold."""
+    g = synth.rng(51)
+    N, K = 6, 384
+    W = synth.weights(N, K, seed=52, heavy=True)
+    s = g.uniform(0.1, 10, size=K).astype(np.float32)
+    q = oracle.quantize_pack(W, s, 128)
+    for n in range(N):
+        for gi in range(K // 128):
+            v = [float(np.float16(float(W[n, k]) * float(s[k])))
+                 for k in range(gi * 128, (gi + 1) * 128)]
+            c, d, z = ex.quantize_group(v)
+            assert q["codes"][n, gi * 128:(gi + 1) * 128].tolist() == c
+            assert Fraction(float(np.uint16(q["scales"][gi, n]).view(np.float16))) == d
+            assert float(np.uint16(q["zeros"][gi, n]).view(np.float16)) == z
+
+
+def test_nonfinite_groups_encoding():
+    """a group with NaN/Inf after the fold gets scale NaN (0x7E00),
+    zero 0, codes 0 and is counted; the others are unaffected."""
+    bad = synth.nonfinite_groups(128)
+    good = synth.weights(1, 128, seed=3)
+    W = np.concatenate([bad, good]).astype(np.float16)
+    q = oracle.quantize_pack(W, None, 128)
+    assert q["nonfinite"] == 3
+    assert q["scales"][0, :3].tolist() == [0x7E00] * 3
+    assert (q["zeros"][0, :3] == 0).all() and (q["codes"][:3] == 0).all()
+    ref = oracle.quantize_pack(good, None, 128)
+    assert q["scales"][0, 3] == ref["scales"][0, 0]
+    # overflow of the fold is non-finite too (O5)
+    q2 = oracle.quantize_pack(np.full((1, 128), 60000, np.float16), np.full(128, 2.0, np.float32))
+    assert q2["nonfinite"] == 1
+    with pytest.raises(ValueError):
+        oracle.quantize_group([1.0, float("nan")])
+
+
+# ---------------------------------------------------------------- Eq. 4
+def test_eq4_loss_properties():
+    """Eq. 4: ≥0; zero on exactly representable W; X×10 -> ×100."""
+    K, N = 128, 8
+    g = synth.rng(61)
+    grid = (g.integers(0, 16, size=(N, K)) - 7) * 0.125
+    grid[:, 0] = -0.875
+    grid[:, 1] = 1.0
+    W = grid.astype(np.float16)
+    q = oracle.quantize_pack(W, None, 128)
+    What = oracle.dequant(q["Wq"], q["scales"], q["zeros"])
+    X = g.normal(size=(4, K))
+    assert oracle.quant_loss(X, W.astype(np.float64), What) == 0.0
+    W2 = synth.weights(N, K, seed=62)
+    q2 = oracle.quantize_pack(W2, None, 128)
+    W2h = oracle.dequant(q2["Wq"], q2["scales"], q2["zeros"])
+    l1 = oracle.quant_loss(X, W2.astype(np.float64), W2h)
+    l10 = oracle.quant_loss(10 * X, W2.astype(np.float64), W2h)
+    assert l1 > 0 and abs(l10 - 100 * l1) <= 1e-9 * l10
+
+
+def test_smoothing_reduces_loss_under_outliers():
+    """smoothing before quantization lowers Eq. 4's loss
+    when activations carry ×100 outlier channels (the paper's core claim, on
+    synthetic data)."""
+    K, N = 512, 256
+    Xc = synth.activations(2048, K, seed=71)
+    W = synth.weights(N, K, seed=72)
+    am = oracle.act_absmax(Xc.astype(np.float16))
+    wm = oracle.weight_absmax(W)
+    X = synth.activations(64, K, seed=73, outlier_seed=71).astype(np.float64)
+    q0 = oracle.quantize_pack(W, None, 128)
+    l_rtn = oracle.quant_loss(X, W.astype(np.float64), oracle.dequant(q0["Wq"], q0["scales"], q0["zeros"]))
+    s = oracle.smooth_scales(wm, am, 0.5)
+    q1 = oracle.quantize_pack(W, s, 128)
+    What_s = oracle.dequant(q1["Wq"], q1["scales"], q1["zeros"]) / s.astype(np.float64)[None, :]
+    l_sq = oracle.quant_loss(X, W.astype(np.float64), What_s)
+    assert l_sq < l_rtn
+
+
+# ---------------------------------------------------------------- P14
+def test_p14_tp_shards():
+    """P14: column shards quantize bit-identically to their rows; group-aligned
+    row shards too; the sum of row-shard partial GEMMs equals the full GEMM."""
+    N, K = 64, 768
+    W = synth.weights(N, K, seed=81)
+    s = synth.rng(82).uniform(0.5, 2, size=K).astype(np.float32)
+    full = oracle.quantize_pack(W, s, 128)
+    col = oracle.quantize_pack(W[16:48], s, 128)
+    assert (col["Wq"] == full["Wq"][16:48]).all()
+    assert (col["scales"] == full["scales"][:, 16:48]).all()
+    row = oracle.quantize_pack(W[:, 256:640], s[256:640], 128)
+    assert (row["Wq"] == full["Wq"][:, 128:320]).all()
+    assert (row["scales"] == full["scales"][2:5]).all()
+    X = synth.activations(4, K, seed=83).astype(np.float16)
+    Y = oracle.gemm(X, full["Wq"], full["scales"], full["zeros"])
+    parts = 0
+    for k0, k1 in ((0, 256), (256, 640), (640, 768)):
+        p = oracle.quantize_pack(W[:, k0:k1], s[k0:k1], 128)
+        parts = parts + oracle.gemm(X[:, k0:k1], p["Wq"], p["scales"], p["zeros"])
+    assert np.allclose(parts, Y, rtol=1e-12, atol=1e-12)
