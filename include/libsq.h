@@ -1,0 +1,160 @@
+/*
+ * libsq.h -- C ABI of the B200-native SmoothQuant+ W4A16 hot path.
+ *
+ * The operations follow the paper's statement of the problem
+ * (/root/reference/PAPER.md, "SmoothQuant+", arxiv 2312.03788):
+ *   Eq. 6  smoothing factors   s_j = max|X_j|^a / max|W_j|^(1-a)
+ *   Eq. 5  weight-side fold    W' = diag(s) W
+ *   Eq. 1    group-wise asymmetric INT4 quantization, g = 128
+ *                             ("Group-size is usually set to be 128")
+ *   Eq. 3  W4A16 linear layer  Y = X^ W^
+ * Readings of points the paper leaves open are in DESIGN.md §3.
+ *
+ * Conventions (all calls):
+ *  - Every tensor pointer is a CUDA DEVICE pointer owned by the caller.  The
+ *    library never allocates device memory, never frees, and never synchronizes
+ *    the host.  Every call is asynchronous on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).
+ *  - Row-major throughout.  Shapes (SURVEY.md §8 notation): M = tokens, K = input
+ *    channels (C_i), N = output channels (C_o), G = K / group.
+ *  - Weights are stored nn.Linear-style W[N][K] (the transpose of Eq. 2's
+ *    W in R^{C_i x C_o}).
+ *  - Packed codes Wq[N][K/2] (uint8): element k of row n is the LOW nibble of byte
+ *    Wq[n][k/2] when k is even, the HIGH nibble when k is odd.
+ *  - scales[G][N] and zeros[G][N] are fp16 bit patterns (uint16), group-major:
+ *    scales[gi][n] is Delta of the group (n, k in [gi*group, (gi+1)*group)).
+ *    zeros hold integers 0..15 stored as fp16.
+ *  - dtype codes: SQ_F16 (IEEE binary16) or SQ_BF16 (bfloat16).
+ *
+ * Errors:
+ *  - Argument errors are detected on the host, return a status and launch
+ *    nothing: NULL pointer -> SQ_ERR_NULL; negative/zero dims -> SQ_ERR_SHAPE
+ *    (M == 0 is a valid no-op); group != 128, K % group != 0 or an unknown dtype
+ *    -> SQ_ERR_UNSUPPORTED; a pointer not 16-byte aligned or N % 8 != 0 ->
+ *    SQ_ERR_ALIGN; a workspace that is too small -> SQ_ERR_WORKSPACE.
+ *  - Launch failures return SQ_ERR_CUDA; sq_last_error() then holds the CUDA
+ *    error string (thread-local).
+ *  - Data-dependent problems (NaN/Inf) are never reported by host sync: see
+ *    nonfinite_count of sq_quantize_pack_groupwise.
+ */
+#ifndef LIBSQ_H
+#define LIBSQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SQ_API __attribute__((visibility("default")))
+#else
+#define SQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int sq_status;
+enum {
+  SQ_OK = 0,
+  SQ_ERR_NULL = 1,
+  SQ_ERR_SHAPE = 2,
+  SQ_ERR_UNSUPPORTED = 3,
+  SQ_ERR_ALIGN = 4,
+  SQ_ERR_CUDA = 5,
+  SQ_ERR_WORKSPACE = 6
+};
+enum { SQ_F16 = 0, SQ_BF16 = 1 };
+enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
+
+/* Library version (major*10000 + minor*100 + patch). */
+SQ_API int sq_version(void);
+/* Static description of a status code. */
+SQ_API const char* sq_status_string(sq_status st);
+/* Detail of the last failure on the calling host thread ("" if none). */
+SQ_API const char* sq_last_error(void);
+/* Largest M served by the decode path under SQ_PATH_AUTO (M_dec). */
+SQ_API int sq_decode_max_m(void);
+
+/*
+ * Calibration statistic of Eq. 6: act_max[k] = max_t |X[t][k]| over the T rows
+ * of a calibration batch X[T][K] (x_dtype).  If `accumulate` is non-zero the
+ * result is max(act_max[k], ...) (running maximum over several batches);
+ * otherwise act_max is overwritten.  NaN in X propagates to act_max.
+ * act_max: fp32[K], device, written.
+ */
+SQ_API sq_status sq_act_absmax(const void* X, int x_dtype, int64_t T, int64_t K,
+                        float* act_max, int accumulate, void* stream);
+
+/*
+ * Eq. 6.  W[N][K] (w_dtype) is the consumer weight; when
+ * several linears share one input (q|k|v, gate|up) the caller passes the
+ * stacked weight, so w_max is the max over all consumers (S11).
+ *   w_max[k] = max_n |W[n][k]|                  (exact)
+ *   s[k] = RN_fp32( max(act_max[k], eps)^alpha / max(w_max[k], eps)^(1-alpha) )
+ * evaluated in fp64; alpha in {0, 0.5, 1} use the exactly rounded forms
+ * 1/w, sqrt(a)/sqrt(w), a; other alpha use fp64 pow (<= 1 ulp fp32 from the
+ * oracle).  alpha must lie in [0, 1] (else SQ_ERR_UNSUPPORTED); eps > 0.
+ * act_max: fp32[K] (>= 0), read.  s_out: fp32[K], written (also used as the
+ * kernel's scratch for w_max, so it must not alias act_max).
+ */
+SQ_API sq_status sq_smooth_scales(const void* W, int w_dtype, int64_t N, int64_t K,
+                           const float* act_max, double alpha, double eps,
+                           float* s_out, void* stream);
+
+/*
+ * Eq. 5 + Eq. 1 (load-time quantization).  For every output
+ * channel n and group gi of `group` consecutive input channels:
+ *   W'[n][k] = RN(W[n][k] * s[k]) to w_dtype, one rounding    (s == NULL: RTN, s = 1)
+ *   lo, hi   = min/max of the group of W';  r = hi - lo (fp64)
+ *   Delta    = RZ_fp16(r / 15); 2^-24 if that underflows to 0;
+ *              constant group c: Delta = 1 if c == 0 else |c|
+ *   Z        = clamp(RHA(-lo / Delta), 0, 15)                  (RHA: half away from 0)
+ *   q        = clamp(RHA(W' / Delta) + Z, 0, 15)
+ * Outputs (device, written): Wq uint8[N][K/2], scales uint16[G][N] (fp16 bits
+ * of Delta), zeros uint16[G][N] (fp16 bits of Z).  Bit-exact with the oracle.
+ * nonfinite_count (device int*, nullable): incremented once per group that holds
+ * NaN/Inf after the fold (or whose r/15 exceeds the fp16 range); such a group is
+ * stored as scale = 0x7E00 (NaN), zero = 0, codes = 0.
+ * s: fp32[K] device or NULL.  Requires group == 128, K % 128 == 0, N % 8 == 0,
+ * 16-byte aligned W/Wq/scales/zeros.
+ */
+SQ_API sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s,
+                                     int64_t N, int64_t K, int group,
+                                     uint8_t* Wq, uint16_t* scales, uint16_t* zeros,
+                                     int* nonfinite_count, void* stream);
+
+/*
+ * Bytes of caller-allocated workspace sq_w4a16_gemm needs for this shape
+ * (may be 0).  The workspace must be zero-filled once before its first use;
+ * every call leaves it zero-filled again.
+ */
+SQ_API size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group);
+
+/*
+ * Eq. 3, W4A16 linear layer:
+ *   Y[m][n] = sum_k X[m][k] * (q[n][k] - Z[gi][n]) * Delta[gi][n],  gi = k / group
+ * fp32 accumulation; Y is written in x_dtype (fp16 or bf16)
+ * "the input and output of all linear layers ... are FP16".
+ * X[M][K], Y[M][N]: device, x_dtype.  Wq/scales/zeros as produced by
+ * sq_quantize_pack_groupwise.  M <= sq_decode_max_m() runs the decode kernel
+ * (mma.sync, split-K over a thread-block cluster), larger M the prefill kernel
+ * (TMA + tcgen05.mma with TMEM operands/accumulators).  One rule, no other
+ * backends.  Y must not alias X.
+ */
+SQ_API sq_status sq_w4a16_gemm(const void* X, int x_dtype,
+                        const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                        void* Y, int64_t M, int64_t N, int64_t K, int group,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same as sq_w4a16_gemm with an explicit path (SQ_PATH_*), for the M sweep and
+ * the parity tests.  SQ_PATH_DECODE requires M <= 16. */
+SQ_API sq_status sq_w4a16_gemm_path(const void* X, int x_dtype,
+                             const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                             void* Y, int64_t M, int64_t N, int64_t K, int group,
+                             void* workspace, size_t workspace_bytes, int path, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIBSQ_H */

@@ -1,0 +1,463 @@
+// K-pre: W4A16 GEMM for large M (prefill) on the 5th-generation tensor cores.
+//
+//   Y[m][n] = sum_k X[m][k] * Ŵ[n][k],  Ŵ = RN((q - Z) * Δ)      PAPER.md:104-106 Eq. 3,
+//                                                             PAPER.md:90 Eq. 1 line 2
+// Design -- "swap-AB, weights in TMEM":
+//  * The MMA computes D[n][m] = Ŵ_tile[n][:] · X_tile[m][:]^T with tcgen05.mma
+//    .cta_group::1.kind::f16, M_mma = 128 weight rows, N_mma = up to 256 tokens,
+//    K = 16 per instruction, fp32 accumulator D in TMEM (256 columns).
+//  * Operand A (the dequantized weights) lives in TMEM: the dequant warps turn
+//    packed codes into fp16/bf16 with register math and write them with
+//    tcgen05.st straight into a 4-stage ring of TMEM A buffers -- the dequantized
+//    tile never touches shared memory, so SMEM bandwidth is spent only on the X
+//    operand (TMA, 128B swizzle) and the packed codes.
+//  * Operand B (activations X[M][K]) is loaded by TMA into a 4-stage SMEM ring in
+//    the canonical K-major SWIZZLE_128B layout the UMMA descriptor expects.
+//  * Packed codes (64 bytes/row/group, SWIZZLE_64B to keep the per-row LDS
+//    conflict-free) and the group's Δ/Z rows arrive by TMA into a separate ring.
+//  * Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA
+//    issuer, warps 4-7 = dequant (thread = TMEM lane = weight row) and epilogue
+//    (tcgen05.ld -> fp16/bf16 -> coalesced stores along n).
+//  * Persistent: one CTA per SM walks the (n-tile, m-tile) list.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "sq_internal.cuh"
+
+namespace sq {
+
+namespace {
+
+constexpr int BM = 128;        // weight rows per tile (MMA M, TMEM lanes)
+constexpr int BT = 256;        // tokens per tile (MMA N max)
+constexpr int BK = 64;         // k per X stage / A stage
+constexpr int kGroup = 128;
+constexpr int NSX = 4;         // X stages (SMEM)
+constexpr int NSC = 4;         // code+scale stages (SMEM), one group each
+constexpr int NSA = 4;         // dequantized-A stages (TMEM)
+constexpr int kThreads = 256;  // 8 warps
+constexpr int kDequantWarp0 = 4;
+
+constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
+constexpr int C_STAGE_BYTES = BM * (kGroup / 2);  // 8 KB
+constexpr int SZ_BYTES = BM * 2;                  // 256 B
+
+constexpr int OFF_X = 0;
+constexpr int OFF_C = OFF_X + NSX * X_STAGE_BYTES;
+constexpr int OFF_S = OFF_C + NSC * C_STAGE_BYTES;
+constexpr int OFF_Z = OFF_S + NSC * SZ_BYTES;
+constexpr int OFF_BAR = OFF_Z + NSC * SZ_BYTES;
+constexpr int NUM_BARS = 2 * NSX + 2 * NSC + 2 * NSA + 2;
+constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16;
+constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;  // slack for 1024 B alignment
+
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t D_COL = 0;      // accumulator: columns [0, 256)
+constexpr uint32_t A_COL = 256;    // A stages: columns [256, 256 + 32*NSA)
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31, %32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),
+      "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),
+      "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups
+// 1024 bytes apart (SBO), sm_100 descriptor version 1.
+__device__ __forceinline__ uint64_t make_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address
+  d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D fp32, A/B fp16 or bf16, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t make_idesc(bool bf16, int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                          // D format f32
+  d |= (bf16 ? 1u : 0u) << 7;            // A format
+  d |= (bf16 ? 1u : 0u) << 10;           // B format
+  d |= (uint32_t)(n >> 3) << 17;         // N >> 3
+  d |= (uint32_t)(BM >> 4) << 24;        // M >> 4
+  return d;
+}
+
+__device__ __forceinline__ uint32_t hsub2_f16(uint32_t a, uint32_t b) {
+  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t hmul2_f16(uint32_t a, uint32_t b) {
+  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// 8 codes (k0..k7, natural order) of one row -> 4 words of Ŵ = RN((q - Z) Δ) pairs
+// (k0,k1), (k2,k3), (k4,k5), (k6,k7) in the MMA's natural k order.
+template <bool kBF16>
+__device__ __forceinline__ void dequant8(uint32_t w, uint32_t zc, uint32_t d2, float df,
+                                         uint32_t* out) {
+  const uint32_t u = w >> 4;
+  const uint32_t sel[4] = {0x4040u, 0x5151u, 0x6262u, 0x7373u};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // low nibble of w.byte(i) -> half 0, low nibble of (w>>4).byte(i) -> half 1
+    const uint32_t p = lop3_and_or(prmt(w, u, sel[i]), 0x000F000Fu, 0x64006400u);
+    const uint32_t qz = hsub2_f16(p, zc);  // exact (q - Z) in fp16
+    if (!kBF16) {
+      out[i] = hmul2_f16(qz, d2);           // RN16((q - Z) Δ)
+    } else {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qz));
+      const __nv_bfloat162 b = __floats2bfloat162_rn(f.x * df, f.y * df);  // exact product, one RN
+      out[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+  }
+}
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
+               uint16_t* __restrict__ Y, int M, int N, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto x_full = [&](int i) { return bar0 + 8u * i; };
+  auto x_empty = [&](int i) { return bar0 + 8u * (NSX + i); };
+  auto c_full = [&](int i) { return bar0 + 8u * (2 * NSX + i); };
+  auto c_empty = [&](int i) { return bar0 + 8u * (2 * NSX + NSC + i); };
+  auto a_full = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + i); };
+  auto a_empty = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + NSA + i); };
+  const uint32_t d_full = bar0 + 8u * (2 * NSX + 2 * NSC + 2 * NSA);
+  const uint32_t d_empty = d_full + 8u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_tiles = (N + BM - 1) / BM;
+  const int m_tiles = (M + BT - 1) / BT;
+  const int num_tiles = n_tiles * m_tiles;
+  const int num_kb = K / BK;
+  const int G = K / kGroup;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
+    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), 4); }
+    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), 4); mbar_init(a_empty(i), 1); }
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_x);
+    prefetch_tmap(&tm_w);
+    prefetch_tmap(&tm_s);
+    prefetch_tmap(&tm_z);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int xs = 0, cs = 0;
+      uint32_t xph = 0, cph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int n0 = (tile / m_tiles) * BM;
+        const int m0 = (tile % m_tiles) * BT;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if ((kb & 1) == 0) {
+            const int g = kb >> 1;
+            mbar_wait(c_empty(cs), cph ^ 1);
+            mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
+            tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
+            tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
+            tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
+            if (++cs == NSC) { cs = 0; cph ^= 1; }
+          }
+          mbar_wait(x_empty(xs), xph ^ 1);
+          mbar_expect_tx(x_full(xs), X_STAGE_BYTES);
+          tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
+          if (++xs == NSX) { xs = 0; xph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      int xs = 0, as = 0;
+      uint32_t xph = 0, aph = 0, dph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % m_tiles) * BT;
+        const int n_mma = min(BT, ((M - m0) + 15) & ~15);
+        const uint32_t idesc = make_idesc(kBF16, n_mma);
+        mbar_wait(d_empty, dph ^ 1);  // epilogue has drained the accumulator
+        dph ^= 1;
+        tc_fence_after();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(a_full(as), aph);
+          mbar_wait(x_full(xs), xph);
+          tc_fence_after();
+          const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t a_tmem = tmem_base + A_COL + (uint32_t)as * (BK / 2) + (uint32_t)kk * 8;
+            const uint64_t bdesc = make_sw128_desc(xaddr + kk * 32);
+            tc_mma_ts(tmem_base + D_COL, a_tmem, bdesc, idesc, (kb | kk) ? 1u : 0u);
+          }
+          tc_commit(x_empty(xs));
+          tc_commit(a_empty(as));
+          if (++xs == NSX) { xs = 0; xph ^= 1; }
+          if (++as == NSA) { as = 0; aph ^= 1; }
+        }
+        tc_commit(d_full);
+      }
+    }
+  } else if (warp >= kDequantWarp0) {
+    // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
+    const int q = warp - kDequantWarp0;  // TMEM sub-partition (warp % 4)
+    const int row = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int cs = 0, as = 0;
+    uint32_t cph = 0, aph = 0, dph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int n0 = (tile / m_tiles) * BM;
+      const int m0 = (tile % m_tiles) * BT;
+      for (int g = 0; g < G; ++g) {
+        mbar_wait(c_full(cs), cph);
+        const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
+        // SWIZZLE_64B: 16-byte chunk c of this row sits at chunk c ^ ((row >> 1) & 3)
+        const int sw = (row >> 1) & 3;
+        uint4 cv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cv[c] = *reinterpret_cast<const uint4*>(crow + ((c ^ sw) << 4));
+        const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
+        const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(c_empty(cs));
+        if (++cs == NSC) { cs = 0; cph ^= 1; }
+
+        const __half zh = __ushort_as_half(zbits);
+        const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), zh));
+        const __half2 d2h = __half2half2(__ushort_as_half(sbits));
+        const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
+        const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
+        const float df = __half2float(__ushort_as_half(sbits));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // two 64-k stages per group
+          const uint32_t words[8] = {cv[2 * h].x,     cv[2 * h].y,     cv[2 * h].z,     cv[2 * h].w,
+                                     cv[2 * h + 1].x, cv[2 * h + 1].y, cv[2 * h + 1].z, cv[2 * h + 1].w};
+          uint32_t a[32];
+#pragma unroll
+          for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+          mbar_wait(a_empty(as), aph ^ 1);
+          tc_fence_after();
+          tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2), a);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full(as));
+          if (++as == NSA) { as = 0; aph ^= 1; }
+        }
+      }
+      // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
+      mbar_wait(d_full, dph);
+      dph ^= 1;
+      tc_fence_after();
+      const int n = n0 + row;
+      const int mt = min(BT, M - m0);
+      for (int c0 = 0; c0 < mt; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
+        tmem_ld_wait();
+        if (n < N) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int m = m0 + c0 + i;
+            if (c0 + i < mt) {
+              const float f = __uint_as_float(v[i]);
+              const uint16_t o = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
+                                       : __half_as_ushort(__float2half_rn(f));
+              Y[(size_t)m * N + n] = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+               CUtensorMapSwizzle sw) {
+  auto fn = get_encode();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t prefill_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
+
+cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                           const uint16_t* zeros, void* Y, int M, int N, int K, void*, size_t,
+                           cudaStream_t st, const char** why) {
+  alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
+  const int G = K / kGroup;
+  bool ok = encode_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_UINT16, X, (uint64_t)K, (uint64_t)M,
+                      (uint64_t)K * 2, BK, BT, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
+                       (uint64_t)K / 2, kGroup / 2, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G,
+                       (uint64_t)N * 2, BM, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)G,
+                       (uint64_t)N * 2, BM, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!ok) {
+    *why = "cuTensorMapEncodeTiled failed";
+    return cudaErrorInvalidValue;
+  }
+  const int num_tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int grid = std::min(num_tiles, num_sms());
+  cudaError_t e;
+  if (x_dtype == SQ_BF16) {
+    e = cudaFuncSetAttribute(prefill_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+    if (e != cudaSuccess) return e;
+    prefill_kernel<true><<<grid, kThreads, SMEM_ALLOC, st>>>(tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K);
+  } else {
+    e = cudaFuncSetAttribute(prefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+    if (e != cudaSuccess) return e;
+    prefill_kernel<false><<<grid, kThreads, SMEM_ALLOC, st>>>(tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sq

@@ -1,0 +1,173 @@
+// libsq C ABI: argument validation and dispatch (include/libsq.h).
+// Host-only code; every kernel launch is asynchronous on the caller's stream.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "sq_internal.cuh"
+
+namespace sq {
+
+static thread_local std::string g_last_error;
+
+static sq_status fail(sq_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+static sq_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return SQ_OK;
+  return fail(SQ_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static bool valid_dtype(int d) { return d == SQ_F16 || d == SQ_BF16; }
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cached[64] = {0};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+constexpr int kDecodeMaxM = 16;
+
+}  // namespace sq
+
+using namespace sq;
+
+extern "C" {
+
+int sq_version(void) { return 100; }
+
+const char* sq_status_string(sq_status st) {
+  switch (st) {
+    case SQ_OK: return "SQ_OK";
+    case SQ_ERR_NULL: return "SQ_ERR_NULL: null pointer argument";
+    case SQ_ERR_SHAPE: return "SQ_ERR_SHAPE: invalid dimension";
+    case SQ_ERR_UNSUPPORTED: return "SQ_ERR_UNSUPPORTED: unsupported group/dtype/shape";
+    case SQ_ERR_ALIGN: return "SQ_ERR_ALIGN: pointer not 16-byte aligned or N % 8 != 0";
+    case SQ_ERR_CUDA: return "SQ_ERR_CUDA: CUDA launch failure";
+    case SQ_ERR_WORKSPACE: return "SQ_ERR_WORKSPACE: workspace too small";
+    default: return "unknown sq_status";
+  }
+}
+
+const char* sq_last_error(void) { return g_last_error.c_str(); }
+
+int sq_decode_max_m(void) { return kDecodeMaxM; }
+
+sq_status sq_act_absmax(const void* X, int x_dtype, int64_t T, int64_t K, float* act_max,
+                        int accumulate, void* stream) {
+  g_last_error.clear();
+  if (!X || !act_max) return fail(SQ_ERR_NULL, "sq_act_absmax: null pointer");
+  if (T < 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_act_absmax: T=%lld K=%lld", (long long)T, (long long)K);
+  if (!valid_dtype(x_dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_act_absmax: dtype %d", x_dtype);
+  if (K % 8 != 0 || !aligned16(X) || !aligned16(act_max))
+    return fail(SQ_ERR_ALIGN, "sq_act_absmax: K %% 8 != 0 or unaligned pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!accumulate) {
+    sq_status s = cuda_status(cudaMemsetAsync(act_max, 0, (size_t)K * sizeof(float), st), "memset");
+    if (s != SQ_OK) return s;
+  }
+  if (T == 0) return SQ_OK;
+  return cuda_status(launch_colabsmax(X, x_dtype, T, K, act_max, st), "colabsmax");
+}
+
+sq_status sq_smooth_scales(const void* W, int w_dtype, int64_t N, int64_t K, const float* act_max,
+                           double alpha, double eps, float* s_out, void* stream) {
+  g_last_error.clear();
+  if (!W || !act_max || !s_out) return fail(SQ_ERR_NULL, "sq_smooth_scales: null pointer");
+  if (N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_smooth_scales: N=%lld K=%lld", (long long)N, (long long)K);
+  if (!valid_dtype(w_dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_scales: dtype %d", w_dtype);
+  if (!(alpha >= 0.0 && alpha <= 1.0) || !(eps > 0.0))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_scales: alpha=%g eps=%g", alpha, eps);
+  if (K % 8 != 0 || !aligned16(W) || !aligned16(s_out) || !aligned16(act_max))
+    return fail(SQ_ERR_ALIGN, "sq_smooth_scales: K %% 8 != 0 or unaligned pointer");
+  if ((const void*)act_max == (const void*)s_out)
+    return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_scales: s_out aliases act_max");
+  cudaStream_t st = (cudaStream_t)stream;
+  sq_status s = cuda_status(cudaMemsetAsync(s_out, 0, (size_t)K * sizeof(float), st), "memset");
+  if (s != SQ_OK) return s;
+  s = cuda_status(launch_colabsmax(W, w_dtype, N, K, s_out, st), "colabsmax");
+  if (s != SQ_OK) return s;
+  return cuda_status(launch_smooth_finalize(act_max, s_out, K, alpha, eps, st), "smooth_finalize");
+}
+
+sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s, int64_t N,
+                                     int64_t K, int group, uint8_t* Wq, uint16_t* scales,
+                                     uint16_t* zeros, int* nonfinite_count, void* stream) {
+  g_last_error.clear();
+  if (!W || !Wq || !scales || !zeros) return fail(SQ_ERR_NULL, "sq_quantize_pack_groupwise: null pointer");
+  if (N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: N=%lld K=%lld", (long long)N, (long long)K);
+  if (group != 128 || K % group != 0 || !valid_dtype(w_dtype))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_quantize_pack_groupwise: group=%d K=%lld dtype=%d", group, (long long)K, w_dtype);
+  if (N % 8 != 0 || !aligned16(W) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
+      (s && !aligned16(s)))
+    return fail(SQ_ERR_ALIGN, "sq_quantize_pack_groupwise: N %% 8 != 0 or unaligned pointer");
+  if (N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: too large");
+  return cuda_status(launch_quantize(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite_count,
+                                     (cudaStream_t)stream), "quantize");
+}
+
+size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group) {
+  (void)group;
+  if (M <= kDecodeMaxM) return 0;
+  return prefill_workspace_bytes(M, N, K);
+}
+
+sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                             const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K,
+                             int group, void* workspace, size_t workspace_bytes, int path,
+                             void* stream) {
+  g_last_error.clear();
+  if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm: null pointer");
+  if (M < 0 || N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+  if (group != 128 || K % group != 0 || !valid_dtype(x_dtype))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
+  if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
+      !aligned16(Y))
+    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm: N %% 8 != 0 or unaligned pointer");
+  if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: too large");
+  if (M == 0) return SQ_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (path == SQ_PATH_AUTO) path = (M <= kDecodeMaxM) ? SQ_PATH_DECODE : SQ_PATH_PREFILL;
+  if (path == SQ_PATH_DECODE) {
+    if (M > kDecodeMaxM) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: decode path needs M <= %d", kDecodeMaxM);
+    DecodePlan p = plan_decode(M, N, K);
+    return cuda_status(launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, p, st), "decode");
+  }
+  if (path == SQ_PATH_PREFILL) {
+    const size_t need = prefill_workspace_bytes(M, N, K);
+    if (need > 0 && (workspace == nullptr || workspace_bytes < need))
+      return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes", need);
+    const char* why = nullptr;
+    cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K,
+                                   workspace, workspace_bytes, st, &why);
+    if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm prefill: %s", why);
+    return cuda_status(e, "prefill");
+  }
+  return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: unknown path %d", path);
+}
+
+sq_status sq_w4a16_gemm(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                        const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K, int group,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  return sq_w4a16_gemm_path(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace,
+                            workspace_bytes, SQ_PATH_AUTO, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal declarations shared by the libsq translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/libsq.h"
+
+namespace sq {
+
+// ---- launchers (each returns the cudaError_t of its launch) ----
+cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K,
+                             float* out_bits_as_float, cudaStream_t st);
+cudaError_t launch_smooth_finalize(const float* act_max, float* s_inout, int64_t K,
+                                   double alpha, double eps, cudaStream_t st);
+cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K,
+                            uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
+                            cudaStream_t st);
+
+struct DecodePlan {
+  int rows_per_cta;   // 64
+  int splits;         // cluster size along K (1..8)
+  int row_blocks;
+};
+DecodePlan plan_decode(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                          const uint16_t* zeros, void* Y, int M, int N, int K,
+                          const DecodePlan& plan, cudaStream_t st);
+
+size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                           const uint16_t* zeros, void* Y, int M, int N, int K,
+                           void* workspace, size_t ws_bytes, cudaStream_t st, const char** why);
+
+int num_sms();
+
+// ---- small device helpers ----
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t and_mask, uint32_t or_mask) {
+  uint32_t r;
+  // r = (a & b) | c   -> immLut = (0xF0 & 0xCC) | 0xAA = 0xEA
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(a), "r"(and_mask), "r"(or_mask));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm volatile("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint16_t ld_u16(const uint16_t* p) {
+  uint16_t r;
+  asm volatile("ld.global.nc.u16 %0, [%1];\n" : "=h"(r) : "l"(p));
+  return r;
+}
+
+}  // namespace sq

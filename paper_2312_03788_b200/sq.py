@@ -1,0 +1,188 @@
+"""Thin Python binding of libsq (include/libsq.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this module
+only turns torch tensors into device pointers and the current CUDA stream, and
+raises on non-OK status.  There is no CPU fallback: if libsq.so is missing the
+import of any entry point raises.
+
+Names follow the C ABI (and the paper's notation):
+  act_absmax(X)                        calibration max|X_j| (Eq. 6 input)
+  smooth_scales(W, act_max, alpha)     Eq. 6 smoothing factors s
+  quantize_pack_groupwise(W, s)        Eq. 5 fold + Eq. 1 INT4 quantize/pack
+  w4a16_gemm(X, Wq, scales, zeros)     Eq. 3 W4A16 linear layer
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libsq.so")
+
+SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
+SQ_F16, SQ_BF16 = 0, 1
+SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
+GROUP = 128
+
+_lib = None
+
+
+class SQError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libsq status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsq.so not built ({LIB_PATH}); run `python -m paper_2312_03788_b200.build`")
+    lib = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    vp, i64, i32, f64, sz = c.c_void_p, c.c_int64, c.c_int, c.c_double, c.c_size_t
+    sig = {
+        "sq_version": (i32, []),
+        "sq_status_string": (c.c_char_p, [i32]),
+        "sq_last_error": (c.c_char_p, []),
+        "sq_decode_max_m": (i32, []),
+        "sq_act_absmax": (i32, [vp, i32, i64, i64, vp, i32, vp]),
+        "sq_smooth_scales": (i32, [vp, i32, i64, i64, vp, f64, f64, vp, vp]),
+        "sq_quantize_pack_groupwise": (i32, [vp, i32, vp, i64, i64, i32, vp, vp, vp, vp, vp]),
+        "sq_w4a16_gemm_workspace_bytes": (sz, [i64, i64, i64, i32]),
+        "sq_w4a16_gemm": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp]),
+        "sq_w4a16_gemm_path": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+EXPORTED = (
+    "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_act_absmax",
+    "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
+    "sq_w4a16_gemm", "sq_w4a16_gemm_path",
+)
+
+
+def lib():
+    return _load()
+
+
+def _check(st: int):
+    if st != SQ_OK:
+        L = _load()
+        raise SQError(st, (L.sq_last_error() or b"").decode() or L.sq_status_string(st).decode())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return SQ_F16
+    if t.dtype == torch.bfloat16:
+        return SQ_BF16
+    raise TypeError(f"unsupported dtype {t.dtype} (need float16/bfloat16)")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libsq entry points take CUDA tensors (device pointers)")
+        if t is not None and not t.is_contiguous():
+            raise ValueError("libsq entry points take contiguous tensors")
+
+
+def version() -> int:
+    return _load().sq_version()
+
+
+def decode_max_m() -> int:
+    return _load().sq_decode_max_m()
+
+
+def act_absmax(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
+               stream=None) -> torch.Tensor:
+    """act_max[k] = max_t |X[t][k]| (calibration statistic of Eq. 6)."""
+    _need_cuda(X)
+    T, K = X.shape
+    if out is None:
+        out = torch.empty(K, dtype=torch.float32, device=X.device)
+    _check(_load().sq_act_absmax(_ptr(X), _dtype_code(X), T, K, _ptr(out), int(accumulate), _stream(stream)))
+    return out
+
+
+def smooth_scales(W: torch.Tensor, act_max: torch.Tensor, alpha: float, eps: float = 1e-5,
+                  out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Eq. 6 smoothing factors s[K] for the (possibly stacked) consumer weight W[N][K]."""
+    _need_cuda(W, act_max)
+    N, K = W.shape
+    if out is None:
+        out = torch.empty(K, dtype=torch.float32, device=W.device)
+    _check(_load().sq_smooth_scales(_ptr(W), _dtype_code(W), N, K, _ptr(act_max), float(alpha),
+                                    float(eps), _ptr(out), _stream(stream)))
+    return out
+
+
+@dataclass
+class QuantizedLinear:
+    """W4 g128 weight: codes [N][K/2] u8, scales/zeros [G][N] fp16 bits (as int16 tensors)."""
+    Wq: torch.Tensor
+    scales: torch.Tensor
+    zeros: torch.Tensor
+    N: int
+    K: int
+    group: int = GROUP
+
+    def nbytes(self) -> int:
+        return self.Wq.numel() + 2 * self.scales.numel() + 2 * self.zeros.numel()
+
+
+def quantize_pack_groupwise(W: torch.Tensor, s: torch.Tensor | None = None, group: int = GROUP,
+                            nonfinite: torch.Tensor | None = None, stream=None) -> QuantizedLinear:
+    """Eq. 5 fold (W' = RN(W·s)) + Eq. 1 group-wise INT4 quantization and packing."""
+    _need_cuda(W, s, nonfinite)
+    N, K = W.shape
+    dev = W.device
+    Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=dev)
+    scales = torch.empty((K // group, N), dtype=torch.int16, device=dev)
+    zeros = torch.empty((K // group, N), dtype=torch.int16, device=dev)
+    _check(_load().sq_quantize_pack_groupwise(_ptr(W), _dtype_code(W), _ptr(s), N, K, group, _ptr(Wq),
+                                              _ptr(scales), _ptr(zeros), _ptr(nonfinite), _stream(stream)))
+    return QuantizedLinear(Wq, scales, zeros, N, K, group)
+
+
+def w4a16_gemm_workspace_bytes(M: int, N: int, K: int, group: int = GROUP) -> int:
+    return int(_load().sq_w4a16_gemm_workspace_bytes(M, N, K, group))
+
+
+def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None, path: int = SQ_PATH_AUTO,
+               stream=None) -> torch.Tensor:
+    """Eq. 3: Y[M][N] = X[M][K] · dequant(q)^T, fp32 accumulate, Y in X's dtype."""
+    _need_cuda(X, out, workspace)
+    M, K = X.shape
+    if K != q.K:
+        raise ValueError(f"K mismatch: X has {K}, weight has {q.K}")
+    if out is None:
+        out = torch.empty((M, q.N), dtype=X.dtype, device=X.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(_load().sq_w4a16_gemm_path(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
+                                      _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes, int(path),
+                                      _stream(stream)))
+    return out

@@ -1,0 +1,97 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/libsq.h declares, and rejects bad arguments on the host before any CUDA
+call (include/libsq.h "Errors")."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2312_03788_b200 import sq
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "libsq.h")).read()
+    return sorted(set(re.findall(r"SQ_API\s+[\w\s\*]+?\b(sq_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(sq.LIB_PATH):
+        from paper_2312_03788_b200 import build
+        build.build()
+    return sq.lib()
+
+
+def test_header_symbols_exported(L):
+    decl = _declared_symbols()
+    assert len(decl) >= 10
+    for name in decl:
+        assert hasattr(L, name), name
+    assert set(decl) == set(sq.EXPORTED)
+
+
+def test_version_and_strings(L):
+    assert L.sq_version() >= 100
+    assert L.sq_decode_max_m() == 16
+    for st in range(7):
+        assert L.sq_status_string(st)
+
+
+FAKE = ctypes.c_void_p(1 << 20)          # 16-byte aligned, never dereferenced
+FAKE_MIS = ctypes.c_void_p((1 << 20) + 2)
+
+
+def _gemm(L, X=FAKE, dt=0, Wq=FAKE, s=FAKE, z=FAKE, Y=FAKE, M=4, N=256, K=512, g=128, path=0):
+    return L.sq_w4a16_gemm_path(X, dt, Wq, s, z, Y, M, N, K, g, None, 0, path, None)
+
+
+def test_gemm_argument_errors(L):
+    assert _gemm(L, X=None) == sq.SQ_ERR_NULL
+    assert b"null" in L.sq_last_error()
+    assert _gemm(L, M=-1) == sq.SQ_ERR_SHAPE
+    assert _gemm(L, N=0) == sq.SQ_ERR_SHAPE
+    assert _gemm(L, K=0) == sq.SQ_ERR_SHAPE
+    assert _gemm(L, g=64) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, K=200) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, dt=7) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, N=252) == sq.SQ_ERR_ALIGN
+    assert _gemm(L, X=FAKE_MIS) == sq.SQ_ERR_ALIGN
+    assert _gemm(L, Y=FAKE_MIS) == sq.SQ_ERR_ALIGN
+    assert _gemm(L, M=17, path=1) == sq.SQ_ERR_UNSUPPORTED   # decode path needs M <= 16
+    assert _gemm(L, path=9) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, M=0) == sq.SQ_OK                           # no-op, no launch
+
+
+def test_quantize_argument_errors(L):
+    q = L.sq_quantize_pack_groupwise
+    assert q(None, 0, None, 8, 128, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_NULL
+    assert q(FAKE, 0, None, 0, 128, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_SHAPE
+    assert q(FAKE, 0, None, 8, 130, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
+    assert q(FAKE, 0, None, 8, 256, 32, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
+    assert q(FAKE, 3, None, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
+    assert q(FAKE, 0, None, 12, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
+    assert q(FAKE, 0, FAKE_MIS, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
+
+
+def test_smooth_argument_errors(L):
+    f = L.sq_smooth_scales
+    assert f(None, 0, 8, 128, FAKE, 0.5, 1e-5, FAKE, None) == sq.SQ_ERR_NULL
+    assert f(FAKE, 0, 8, 0, FAKE, 0.5, 1e-5, FAKE, None) == sq.SQ_ERR_SHAPE
+    assert f(FAKE, 0, 8, 128, FAKE, 1.5, 1e-5, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_UNSUPPORTED
+    assert f(FAKE, 0, 8, 128, FAKE, 0.5, 0.0, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_UNSUPPORTED
+    assert f(FAKE, 0, 8, 128, FAKE, 0.5, 1e-5, FAKE, None) == sq.SQ_ERR_UNSUPPORTED  # aliasing
+    assert f(FAKE, 0, 8, 124, FAKE, 0.5, 1e-5, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_ALIGN
+    a = L.sq_act_absmax
+    assert a(None, 0, 4, 128, FAKE, 0, None) == sq.SQ_ERR_NULL
+    assert a(FAKE, 0, -1, 128, FAKE, 0, None) == sq.SQ_ERR_SHAPE
+
+
+def test_workspace_query(L):
+    assert L.sq_w4a16_gemm_workspace_bytes(1, 8192, 8192, 128) == 0
+    assert L.sq_w4a16_gemm_workspace_bytes(2048, 8192, 8192, 128) >= 0
