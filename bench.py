@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the SmoothQuant+ W4A16 hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...      (N > 1, one rank per GPU)
+
+Workload (BASELINE.json metric "W4A16 GEMM: decode HBM GB/s & prefill TFLOP/s vs
+roofline, Code Llama-34B shapes"): the W4A16 linear stack of Code Llama-34B --
+48 decoder layers x {qkv 8192->10240, o_proj 8192->8192, gate|up 8192->44032,
+down 22016->8192} (17.66 GB of W4 g128 weights, larger than L2 by 140x).
+
+  step   = one decode pass of the whole stack at each M in --decode-m (default
+           1,4,16 -- BASELINE.json configs[1]/[3] batch sizes), i.e. every W4A16
+           GEMM of the model for one token batch, replayed as one CUDA graph.
+  value  = algorithmic bytes (K*N/2 + 4*N*K/128 + 2*M*K + 2*M*N per GEMM, summed
+           over all ranks) / max-over-ranks device time -> GB/s.
+  prefill= the same stack's layers at M = 2048 (configs[2]) -> TFLOP/s (sub-object).
+  quantize = Eq. 6 smoothing + Eq. 1 quantize/pack of one layer (a1-a4) -> GB/s.
+  N > 1  = tensor parallel (column qkv/gate|up, row o/down + NCCL all-reduce),
+           the same total model split over N ranks ("scaling": "strong").
+
+The reference arm (--impl reference) times the fp64 CPU oracle (oracle/) on host
+cores on a bounded sample of the same decode workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W4A16 GEMM: decode HBM GB/s & prefill TFLOP/s vs roofline, Code Llama-34B shapes"
+UNIT = "GB/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--layers", type=int, default=48)
+    ap.add_argument("--decode-m", type=str, default="1,4,16")
+    ap.add_argument("--prefill-m", type=int, default=2048)
+    ap.add_argument("--prefill-layers", type=int, default=4)
+    ap.add_argument("--skip-prefill", action="store_true")
+    ap.add_argument("--skip-quant", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+def load_ncu_traffic(kernel_key: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.idx)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.1)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), power=float(parts[3]),
+                                 hw=parts[5], hwt=parts[6], swt=parts[7], swp=parts[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("swp", "sw_power_cap")):
+                if r[k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows),
+                "sm_max_mhz": max(r["smax"] for r in rows),
+                "power_w_max": max(r["power"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- CPU oracle legs
+def oracle_decode_sample(ms, rows=1024, K=8192, seed=1234):
+    """Time the fp64 oracle's W4A16 GEMM (dequant + fp64 matmul) on `rows` output
+    channels of a 34B o_proj-shaped layer at each M; returns (bytes, seconds, desc)."""
+    import numpy as np
+
+    import oracle
+    g = np.random.Generator(np.random.PCG64(seed))
+    Wq = g.integers(0, 256, size=(rows, K // 2), dtype=np.uint8)
+    scales = (g.uniform(1e-4, 1e-2, size=(K // 128, rows))).astype(np.float16).view(np.uint16)
+    zeros = g.integers(0, 16, size=(K // 128, rows)).astype(np.float16).view(np.uint16)
+    total_b, total_t = 0, 0.0
+    for M in ms:
+        X = g.normal(size=(M, K)).astype(np.float16)
+        t0 = time.perf_counter()
+        Y = oracle.gemm(X, Wq, scales, zeros, 128)
+        total_t += time.perf_counter() - t0
+        assert Y.shape == (M, rows)
+        total_b += K * rows // 2 + 4 * rows * (K // 128) + 2 * M * K + 2 * M * rows
+    desc = f"oracle.gemm (fp64 dequant + numpy fp64 matmul) on {rows} output channels of a " \
+           f"K={K} layer at M={','.join(map(str, ms))}"
+    return total_b, total_t, desc
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(a, rank):
+    if rank != 0:
+        return
+    ms = [int(x) for x in a.decode_m.split(",")]
+    for _ in range(a.warmup):
+        oracle_decode_sample(ms, rows=512)
+    tot_b, tot_t, desc = 0, 0.0, ""
+    for _ in range(a.steps):
+        b, t, desc = oracle_decode_sample(ms, rows=512)
+        tot_b += b
+        tot_t += t
+    v = tot_b / tot_t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot_t / a.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "codellama-34b-w4a16-linear-stack-decode", "decode_m": ms,
+                   "sample": "o_proj-shaped layer, 512 output channels per step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_03788_b200 import sq, stack, tp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    peaks, peaks_src = load_peaks()
+    ms = [int(x) for x in a.decode_m.split(",")]
+    model = tp.CODELLAMA_34B
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # ---------------- decode stack (the headline)
+    st = stack.build_stack(model, a.layers, rank, world, dev, group=pg)
+    bufs = [stack.make_buffers(st, M, dev) for M in ms]
+    if world > 1:
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)  # NCCL communicator up before graph capture
+    launches = {"n": 0}
+
+    def step_eager():
+        n = 0
+        for b in bufs:
+            n += stack.run_pass(st, b)
+        return n
+
+    launches_per_step = step_eager()
+    torch.cuda.synchronize()
+    graph = None
+    if not a.no_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step_eager()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_eager()
+        torch.cuda.synchronize()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step_eager()
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gpu_index = int((os.environ.get("CUDA_VISIBLE_DEVICES") or str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(gpu_index) as clk:
+        ev0.record()
+        for _ in range(a.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    t_rank = ev0.elapsed_time(ev1) * 1e-3
+    t = max_over_ranks(t_rank)
+    bytes_rank = sum(stack.pass_bytes(st, M) for M in ms)
+    bytes_all = sum_over_ranks(float(bytes_rank))
+    value = bytes_all * a.steps / t / 1e9
+    clocks = clk.summary()
+
+    # dominant kernel = the decode GEMM: every launch in the step is one; per-rank
+    # algorithmic bytes per launch / average launch duration (CUDA events, same stream)
+    dec_launch_s = t_rank / (a.steps * launches_per_step)
+    dec_bytes_launch = bytes_rank / launches_per_step
+    hbm_peak = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    achieved = dec_bytes_launch / dec_launch_s / 1e9
+    traffic = load_ncu_traffic("decode")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "kernel": "sq::decode_kernel (mma.sync W4A16, cluster split-K)",
+                "peak_source": f"{peaks_src} hbm_gbs", "bytes_per_launch": dec_bytes_launch}
+
+    # per-M breakdown (graph per M), for the report
+    per_m = {}
+    for b in bufs:
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            stack.run_pass(st, b)
+        for _ in range(2):
+            g2.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, a.steps // 3)
+        e0.record()
+        for _ in range(reps):
+            g2.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        tm = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / reps)
+        bm = sum_over_ranks(float(stack.pass_bytes(st, b.M)))
+        per_m[str(b.M)] = {"ms_per_pass": tm * 1e3, "GB/s": bm / tm / 1e9,
+                           "frac_hbm": bm / tm / 1e9 / hbm_peak / world}
+        del g2
+
+    # ---------------- end to end through the public API (host buffers)
+    e2e = None
+    if not a.skip_e2e:
+        hx = {b.M: {k: v.cpu().pin_memory() for k, v in b.x.items()} for b in bufs}
+        hy = {b.M: {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in b.y.items()}
+              for b in bufs}
+        h2d = sum(v.numel() * v.element_size() for d in hx.values() for v in d.values())
+        d2h = sum(v.numel() * v.element_size() for d in hy.values() for v in d.values())
+
+        def e2e_step():
+            for b in bufs:
+                for k, v in hx[b.M].items():
+                    b.x[k].copy_(v, non_blocking=True)
+                stack.run_pass(st, b)
+                for k, v in hy[b.M].items():
+                    v.copy_(b.y[k], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, a.steps // 3)
+        e0.record()
+        for _ in range(reps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        te = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+        e2e = {"value": bytes_all * reps / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "api": "paper_2312_03788_b200.sq.w4a16_gemm (ctypes -> "
+               "sq_w4a16_gemm), eager launches, pinned host<->device copies each step"}
+
+    del graph
+    torch.cuda.empty_cache()
+
+    # ---------------- prefill (a7)
+    prefill = None
+    if not a.skip_prefill:
+        M = a.prefill_m
+        pst = stack.LinearStack(model, rank, world, layers=st.layers[: a.prefill_layers], group=pg)
+        pb = stack.make_buffers(pst, M, dev)
+        nbytes = sq.w4a16_gemm_workspace_bytes(M, 8192, 22016)
+        ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            stack.run_pass(pst, pb, workspace=ws)
+        barrier()
+        reps = max(3, a.steps // 5)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            stack.run_pass(pst, pb, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        tp_rank = e0.elapsed_time(e1) * 1e-3 / reps
+        tpre = max_over_ranks(tp_rank)
+        flops_rank = stack.pass_flops(pst, M)
+        flops_all = sum_over_ranks(float(flops_rank))
+        tf = flops_all / tpre / 1e12
+        tc_peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])  # fp16 dense == bf16 dense
+        n_l = len(pst.layers) * len(pst.shards)
+        ach = flops_rank / tp_rank / 1e12
+        prefill = {"value": tf, "unit": "TFLOP/s", "M": M, "layers": len(pst.layers),
+                   "ms_per_pass": tpre * 1e3,
+                   "roofline": {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
+                                "frac": ach / tc_peak, "traffic": load_ncu_traffic("prefill"),
+                                "kernel": "sq::prefill_kernel (TMA + tcgen05.mma, A in TMEM)",
+                                "peak_source": f"{peaks_src} bf16_tflops (fp16 dense = bf16 dense)",
+                                "flops_per_launch": flops_rank / n_l}}
+        del pb, ws
+        torch.cuda.empty_cache()
+
+    # ---------------- load-time smoothing + quantization (a1-a4)
+    quant = None
+    if not a.skip_quant:
+        Ws, ams = [], []
+        for si, sh in enumerate(st.shards):
+            Ws.append(stack.synth_weight(sh.N, sh.K, 99 + si, dev))
+            ams.append(stack.synth_act_max(sh.K, 5 + si, dev))
+        svec = [torch.empty(sh.K, device=dev) for sh in st.shards]
+
+        def qstep():
+            for W, am, s in zip(Ws, ams, svec):
+                sq.smooth_scales(W, am, 0.5, out=s)
+                sq.quantize_pack_groupwise(W, s)
+
+        for _ in range(2):
+            qstep()
+        barrier()
+        reps = max(3, a.steps // 5)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            qstep()
+        e1.record()
+        torch.cuda.synchronize()
+        tq = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / reps)
+        qb = sum(2 * W.numel() + 4 * W.shape[1] * 2 + 2 * W.numel() + W.numel() // 2
+                 + 4 * W.shape[0] * (W.shape[1] // 128) for W in Ws)
+        qb_all = sum_over_ranks(float(qb))
+        quant = {"value": qb_all / tq / 1e9, "unit": "GB/s", "ms_per_layer": tq * 1e3,
+                 "what": "sq_smooth_scales (w_max + Eq. 6) + sq_quantize_pack_groupwise for one layer"}
+        del Ws
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.skip_cpu:
+        b_tot, t_tot, desc = 0, 0.0, ""
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < 12.0:
+            b, tt, desc = oracle_decode_sample(ms, rows=1024)
+            b_tot += b
+            t_tot += tt
+        cpu = {"value": b_tot / t_tot / 1e9, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "sample": desc + f"; repeated for {t_tot:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "codellama-34b-w4a16-linear-stack-decode", "layers": a.layers,
+                       "decode_m": ms, "group": 128, "linears": [s.name for s in st.shards],
+                       "parallelism": f"tp{world}" if world > 1 else "none",
+                       "weights_bytes_per_step_all_ranks": bytes_all,
+                       "l2": "no flush: every pass streams the stack's weights (GBs) > 126 MB L2",
+                       "graph": graph is not None or not a.no_graph},
+            "gpu_launches": launches_per_step * a.steps,
+            "clocks": clocks,
+            "roofline": roofline,
+            "per_m": per_m,
+            "prefill": prefill,
+            "quantize": quant,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

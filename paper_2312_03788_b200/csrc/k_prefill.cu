@@ -184,7 +184,7 @@ template <bool kBF16>
 __device__ __forceinline__ void dequant8(uint32_t w, uint32_t zc, uint32_t d2, float df,
                                          uint32_t* out) {
   const uint32_t u = w >> 4;
-  const uint32_t sel[4] = {0x4040u, 0x5151u, 0x6262u, 0x7373u};
+  const uint32_t sel[4] = {0x0400u, 0x0501u, 0x0602u, 0x0703u};  // byte i of w -> b0, of w>>4 -> b2
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     // low nibble of w.byte(i) -> half 0, low nibble of (w>>4).byte(i) -> half 1

@@ -134,6 +134,7 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
                              int group, void* workspace, size_t workspace_bytes, int path,
                              void* stream) {
   g_last_error.clear();
+  if (M == 0 && N > 0 && K > 0) return SQ_OK;  // no-op; X/Y may be empty (null) tensors
   if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm: null pointer");
   if (M < 0 || N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
   if (group != 128 || K % group != 0 || !valid_dtype(x_dtype))

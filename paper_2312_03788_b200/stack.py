@@ -1,0 +1,118 @@
+"""The Code Llama W4A16 linear stack on one rank: synthetic weights quantized on the
+device (PAPER.md:176 load-time quantization), and decode / prefill passes through
+sq_w4a16_gemm with an all-reduce after the row-parallel layers.
+
+Attention, RMSNorm, SiLU and the residual stream are not part of the hot path
+(SURVEY.md §3 (5)): each linear reads a fixed, pre-filled activation buffer of the
+right shape, so a pass streams exactly the W4 weights of every layer once.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import sq
+from .tp import CODELLAMA_34B, LinearShard, ModelShape, decode_bytes, gemm_flops, layer_shards
+
+
+@dataclass
+class Linear:
+    shard: LinearShard
+    q: sq.QuantizedLinear
+
+
+@dataclass
+class LinearStack:
+    model: ModelShape
+    rank: int
+    world: int
+    layers: list = field(default_factory=list)   # list[list[Linear]]
+    group: object = None                          # torch.distributed process group (None: no AR)
+    dtype: torch.dtype = torch.float16
+
+    @property
+    def shards(self) -> list[LinearShard]:
+        return [l.shard for l in self.layers[0]]
+
+
+def synth_weight(N: int, K: int, seed: int, device, dtype=torch.float16) -> torch.Tensor:
+    """W ~ N(0, 0.02^2) drawn on the device with a seeded generator (synthetic
+    stand-in for a Code Llama checkpoint)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return (torch.randn((N, K), generator=g, device=device, dtype=torch.float32) * 0.02).to(dtype)
+
+
+def synth_act_max(K: int, seed: int, device) -> torch.Tensor:
+    """Per-channel calibration maxima with 8 x100 outlier channels."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    a = 3.0 + torch.rand(K, generator=g, device=device)
+    idx = torch.randperm(K, generator=g, device=device)[:8]
+    a[idx] *= 100.0
+    return a.float().contiguous()
+
+
+def build_stack(model: ModelShape = CODELLAMA_34B, layers: int | None = None, rank: int = 0,
+                world: int = 1, device="cuda", seed: int = 1234, smooth: bool = True,
+                group=None) -> LinearStack:
+    """Quantize `layers` decoder layers' linears for this rank.  Each rank draws only its
+    own shard; smoothing factors are computed on the shard (setup only, not timed)."""
+    L = model.layers if layers is None else layers
+    st = LinearStack(model, rank, world, group=group)
+    shards = layer_shards(model, rank, world)
+    for li in range(L):
+        row = []
+        for si, sh in enumerate(shards):
+            W = synth_weight(sh.N, sh.K, seed + 1000 * li + 10 * si + 100000 * rank, device)
+            s = None
+            if smooth:
+                am = synth_act_max(sh.K, seed + 7 * si, device)
+                s = sq.smooth_scales(W, am, 0.5)
+            row.append(Linear(sh, sq.quantize_pack_groupwise(W, s)))
+            del W
+        st.layers.append(row)
+    return st
+
+
+@dataclass
+class PassBuffers:
+    M: int
+    x: dict      # shard name -> input [M][K_r]
+    y: dict      # shard name -> output [M][N_r]
+
+
+def make_buffers(st: LinearStack, M: int, device="cuda", seed: int = 7) -> PassBuffers:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + M)
+    xs, ys = {}, {}
+    for sh in st.shards:
+        xs[sh.name] = torch.randn((M, sh.K), generator=g, device=device).to(st.dtype)
+        ys[sh.name] = torch.empty((M, sh.N), device=device, dtype=st.dtype)
+    return PassBuffers(M, xs, ys)
+
+
+def run_pass(st: LinearStack, buf: PassBuffers, path: int = sq.SQ_PATH_AUTO, workspace=None) -> int:
+    """One pass of every layer's linears at buf.M tokens; returns #kernel launches."""
+    import torch.distributed as dist
+
+    n = 0
+    for row in st.layers:
+        for lin in row:
+            y = buf.y[lin.shard.name]
+            sq.w4a16_gemm(buf.x[lin.shard.name], lin.q, out=y, path=path, workspace=workspace)
+            n += 1
+            if lin.shard.allreduce and st.group is not None:
+                dist.all_reduce(y, group=st.group)
+    return n
+
+
+def pass_bytes(st: LinearStack, M: int) -> int:
+    """Algorithmic HBM bytes of one pass on this rank."""
+    return len(st.layers) * sum(decode_bytes(M, sh.K, sh.N) for sh in st.shards)
+
+
+def pass_flops(st: LinearStack, M: int) -> int:
+    return len(st.layers) * sum(gemm_flops(M, sh.K, sh.N) for sh in st.shards)
