@@ -360,6 +360,7 @@ def main():
                "d2h_bytes_per_step": d2h, "api": "paper_2312_03788_b200.sq.w4a16_gemm (ctypes -> "
                "sq_w4a16_gemm), eager launches, pinned host<->device copies each step"}
 
+    used_graph = graph is not None
     del graph
     torch.cuda.empty_cache()
 
@@ -453,7 +454,7 @@ def main():
                        "parallelism": f"tp{world}" if world > 1 else "none",
                        "weights_bytes_per_step_all_ranks": bytes_all,
                        "l2": "no flush: every pass streams the stack's weights (GBs) > 126 MB L2",
-                       "graph": graph is not None or not a.no_graph},
+                       "cuda_graph": used_graph},
             "gpu_launches": launches_per_step * a.steps,
             "clocks": clocks,
             "roofline": roofline,

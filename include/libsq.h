@@ -124,9 +124,11 @@ SQ_API sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const fl
                                      int* nonfinite_count, void* stream);
 
 /*
- * Bytes of caller-allocated workspace sq_w4a16_gemm needs for this shape
- * (may be 0).  The workspace must be zero-filled once before its first use;
- * every call leaves it zero-filled again.
+ * Bytes of caller-allocated device workspace sq_w4a16_gemm needs for this shape
+ * (the decode path's stream-K fixup: per-row-block counters + fp32 partial tiles).
+ * The workspace must be 16-byte aligned and zero-filled once before its first
+ * use; every call leaves it zero-filled again.  Calls that may run concurrently
+ * (different streams) need different workspaces.
  */
 SQ_API size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group);
 
@@ -137,7 +139,7 @@ SQ_API size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int
  * "the input and output of all linear layers ... are FP16".
  * X[M][K], Y[M][N]: device, x_dtype.  Wq/scales/zeros as produced by
  * sq_quantize_pack_groupwise.  M <= sq_decode_max_m() runs the decode kernel
- * (mma.sync, split-K over a thread-block cluster), larger M the prefill kernel
+ * (TMA-fed mma.sync, persistent stream-K over K), larger M the prefill kernel
  * (TMA + tcgen05.mma with TMEM operands/accumulators).  One rule, no other
  * backends.  Y must not alias X.
  */

@@ -4,39 +4,113 @@
 //   PAPER.md:104-106 Eq. 3 with Ŵ of Eq. 1 line 2; fp32 accumulation.
 //
 // Design:
-//  * A warp owns 16 output channels; lane (r = lane/4, j = lane%4) streams 16 bytes
-//    (32 codes) of row r and 16 bytes of row r+8 per group with 128-bit
-//    ld.global.nc.L1::no_allocate loads (4 lanes -> 64 contiguous bytes per row).
-//    One (16-row x 128-k) group = two loads per lane = 8 mma.sync.m16n8k16.
-//  * Register dequant to the EXACT integer (q - Z) in fp16/bf16 with the
-//    lop3 magic-number trick; Δ is applied once per group to the fp32 accumulator
-//    fragment (so the MMA sees exact operands and only fp32 rounding remains).
-//  * The MMA's k order is permuted (nibble pairs (e0,e4),(e1,e5),...): X is loaded in
-//    natural order (L1-resident, shared by all warps) and permuted with PRMT.
-//  * Tokens are the MMA's N = 8 (MT = 2 tiles for M <= 16).
-//  * Split-K over a thread-block cluster of S CTAs along K; the S fp32 partial
-//    tiles are reduced through distributed shared memory by the cluster's rank-0
-//    CTA in fixed rank order (deterministic, no global workspace, no atomics).
+//  * Persistent stream-K: the (64-row block x 4-group stage) units of the whole GEMM
+//    are split into equal contiguous ranges, one per resident CTA (one wave, no
+//    tail); a row block cut between CTAs is finished by a deterministic fixup (the
+//    last contributor sums the fp32 partials in CTA order).
+//  * One producer warp streams each unit with TMA into a 4-stage SMEM ring: packed
+//    codes (3-D box 64 B x 64 rows x 4 groups), the scale/zero rows and the matching
+//    X slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free) --
+//    about 100 KB per SM in flight, which is what HBM's latency-bandwidth product
+//    asks for.
+//  * Four consumer warps: warp w takes group w of every stage for all 64 rows (4
+//    row tiles of 16), so its X fragment is loaded (and k-permuted with PRMT) once
+//    and reused four times.  Codes are turned into the EXACT integer (q - Z) in
+//    fp16/bf16 with the lop3 magic-number trick and fed to mma.sync.m16n8k16 with
+//    fp32 accumulation; Δ is applied once per group to the accumulator fragment.
+//  * Row-block results of the 4 consumer warps are summed through shared memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
-#include <cooperative_groups.h>
+#include <mutex>
 
 #include "sq_internal.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace sq {
 
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kThreads = kWarps * 32;
-constexpr int kRowsPerCta = kWarps * 16;
 constexpr int kGroup = 128;
+constexpr int BN = 64;          // rows per row block
+constexpr int GPS = 4;          // groups per stage (= consumer warps)
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kMaxCtasPerSm = 2;
 
-struct WFrag {
-  uint4 a, b;       // 32 codes of row r and of row r+8
-  uint32_t sa, sb;  // (scale bits) | (zero bits << 16) for rows r and r+8
+template <int MT>
+struct Cfg {
+  static constexpr int MPAD = 8 * MT;
+  static constexpr int NS = MT == 1 ? 4 : 3;
+  static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB
+  static constexpr int XB = GPS * MPAD * kGroup * 2;      // 8 / 16 KB
+  static constexpr int SZ = GPS * BN * 2;                 // 512 B
+  static constexpr int STAGE = CODES + XB + 2 * SZ;
+  static constexpr int OFF_RED = NS * STAGE;
+  static constexpr int RED = (kConsumerWarps - 1) * MPAD * BN * 4;
+  static constexpr int OFF_BAR = OFF_RED + RED;
+  static constexpr int OFF_FLAG = OFF_BAR + 2 * NS * 8;
+  static constexpr int SMEM = OFF_FLAG + 16;
+  static constexpr int SMEM_ALLOC = SMEM + 1024;
 };
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr));
+  return v;
+}
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                           uint32_t a3, uint32_t b0, uint32_t b1, bool bf16) {
@@ -64,266 +138,393 @@ __device__ __forceinline__ uint32_t hsub2_u(uint32_t a, uint32_t b, bool bf16) {
   __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
   return *reinterpret_cast<uint32_t*>(&r);
 }
-
 __device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
   __half2 r = __hfma2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b),
                       *reinterpret_cast<__half2*>(&c));
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
-// Dequantize one 32-bit word (8 codes, k offsets 0..7) of one row into the four
-// exact (q - Z) pairs (e0,e4), (e1,e5), (e2,e6), (e3,e7).
+// One 32-bit word of codes (k offsets 0..7 of one row) -> the exact (q - Z) pairs
+// (e0,e4), (e1,e5), (e2,e6), (e3,e7) in fp16 / bf16.
 template <bool kBF16>
-__device__ __forceinline__ void dequant_word(uint32_t w, uint32_t zsub, uint32_t zfma,
-                                             uint32_t (&h)[4]) {
+__device__ __forceinline__ void dequant_word(uint32_t w, uint32_t zsub, uint32_t zfma, uint32_t (&h)[4]) {
   if (!kBF16) {
     const uint32_t t = w >> 8;
-    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x64006400u), zsub, false);   // 1024+e0,e4
-    h[2] = hsub2_u(lop3_and_or(t, 0x000F000Fu, 0x64006400u), zsub, false);   // 1024+e2,e6
-    // 1024+16e1 -> (x/16) - (64+Z)
-    h[1] = hfma2_u(lop3_and_or(w, 0x00F000F0u, 0x64006400u), 0x2C002C00u, zfma);
+    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x64006400u), zsub, false);  // 1024+q - (1024+Z)
+    h[2] = hsub2_u(lop3_and_or(t, 0x000F000Fu, 0x64006400u), zsub, false);
+    h[1] = hfma2_u(lop3_and_or(w, 0x00F000F0u, 0x64006400u), 0x2C002C00u, zfma);  // (1024+16q)/16-(64+Z)
     h[3] = hfma2_u(lop3_and_or(t, 0x00F000F0u, 0x64006400u), 0x2C002C00u, zfma);
   } else {
-    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x43004300u), zsub, true);   // 128+e0,e4
+    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x43004300u), zsub, true);  // 128+q - (128+Z)
     h[1] = hsub2_u(lop3_and_or(w >> 4, 0x000F000Fu, 0x43004300u), zsub, true);
     h[2] = hsub2_u(lop3_and_or(w >> 8, 0x000F000Fu, 0x43004300u), zsub, true);
     h[3] = hsub2_u(lop3_and_or(w >> 12, 0x000F000Fu, 0x43004300u), zsub, true);
   }
 }
 
+// zero-point constants from the fp16 bits of Z (an integer 0..15)
 template <bool kBF16>
-__device__ __forceinline__ void zero_consts(uint32_t szbits, uint32_t& zsub, uint32_t& zfma,
-                                            float& d) {
-  const __half z = __ushort_as_half((unsigned short)(szbits >> 16));
-  d = __half2float(__ushort_as_half((unsigned short)(szbits & 0xFFFFu)));
+__device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint32_t& zfma) {
+  const uint32_t z = (uint32_t)__half2int_rn(__ushort_as_half(zbits));
   if (!kBF16) {
-    const __half c1 = __hadd(__float2half(1024.0f), z);           // exact
-    const __half c2 = __hneg(__hadd(__float2half(64.0f), z));     // exact
-    const __half2 p1 = __half2half2(c1), p2 = __half2half2(c2);
-    zsub = *reinterpret_cast<const uint32_t*>(&p1);
-    zfma = *reinterpret_cast<const uint32_t*>(&p2);
+    const uint32_t c1 = 0x6400u + z;          // fp16(1024 + Z): ulp of 1024 is 1
+    const uint32_t c2 = 0xD400u + (z << 4);   // fp16(-(64 + Z)): ulp of 64 is 1/16
+    zsub = c1 | (c1 << 16);
+    zfma = c2 | (c2 << 16);
   } else {
-    const __nv_bfloat16 c1 = __float2bfloat16_rn(128.0f + __half2float(z));  // exact (<= 143)
-    const __nv_bfloat162 p1 = __bfloat162bfloat162(c1);
-    zsub = *reinterpret_cast<const uint32_t*>(&p1);
+    const uint32_t c1 = 0x4300u + z;          // bf16(128 + Z): ulp of 128 is 1
+    zsub = c1 | (c1 << 16);
     zfma = 0;
   }
 }
 
+struct Work {
+  int units, upb, cta_q, cta_r;  // total units, units per row block, units per CTA (q, remainder)
+  __device__ int start(int c) const { return c * cta_q + min(c, cta_r); }
+  __device__ int cta_of(int u) const {
+    const int big = (cta_q + 1) * cta_r;
+    return u < big ? u / (cta_q + 1) : cta_r + (u - big) / cta_q;
+  }
+};
+
 template <int MT, bool kBF16>
-__global__ void __launch_bounds__(kThreads)
-decode_kernel(const uint16_t* __restrict__ X, const uint8_t* __restrict__ Wq,
-              const uint16_t* __restrict__ scales, const uint16_t* __restrict__ zeros,
-              uint16_t* __restrict__ Y, int M, int N, int K, int splits) {
-  __shared__ float part[MT * 8][kRowsPerCta];
+__global__ void __launch_bounds__(kThreads, kMaxCtasPerSm)
+decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+              const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
+              uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
+              int M, int N, Work wk) {
+  using C = Cfg<MT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase + C::OFF_BAR;
+  const uint32_t bar_empty = bar_full + 8 * C::NS;
+  volatile int* flag = reinterpret_cast<volatile int*>(smem + C::OFF_FLAG);
+  float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r = lane / 4, j = lane % 4;
-  const int split = blockIdx.x;  // == rank in the cluster (cluster dims = (splits,1,1))
-  const int n0 = blockIdx.y * kRowsPerCta + warp * 16;
-  const int rowA = n0 + r, rowB = n0 + r + 8;
-  const bool okA = rowA < N, okB = rowB < N;
-  const int G = K / kGroup;
-  const int gbeg = (int)(((long long)G * split) / splits);
-  const int gend = (int)(((long long)G * (split + 1)) / splits);
+  const int c = blockIdx.x;
+  const int u0 = wk.start(c), u1 = wk.start(c + 1);
 
-  const uint8_t* pA = Wq + (size_t)rowA * (K / 2) + j * 16;
-  const uint8_t* pB = Wq + (size_t)rowB * (K / 2) + j * 16;
-
-  auto load = [&](int g) {
-    WFrag f;
-    if (okA) {
-      f.a = ld_nc_v4(pA + (size_t)g * 64);
-      f.sa = (uint32_t)ld_u16(scales + (size_t)g * N + rowA) |
-             ((uint32_t)ld_u16(zeros + (size_t)g * N + rowA) << 16);
-    } else {
-      f.a = make_uint4(0, 0, 0, 0);
-      f.sa = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(bar_full + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, kConsumerWarps);
     }
-    if (okB) {
-      f.b = ld_nc_v4(pB + (size_t)g * 64);
-      f.sb = (uint32_t)ld_u16(scales + (size_t)g * N + rowB) |
-             ((uint32_t)ld_u16(zeros + (size_t)g * N + rowB) << 16);
-    } else {
-      f.b = make_uint4(0, 0, 0, 0);
-      f.sb = 0;
-    }
-    return f;
-  };
-
-  float acc[MT][4];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[mt][i] = 0.0f;
-
-  auto compute = [&](const WFrag& f, int g) {
-    // X fragments: token t = r + 8 mt, k = g*128 + 32 j + [0, 32)
-    uint32_t xv[MT][16];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int t = r + 8 * mt;
-      if (t < M) {
-        const uint4* xp = reinterpret_cast<const uint4*>(X + (size_t)t * K + (size_t)g * kGroup + j * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 v = __ldg(xp + q);
-          xv[mt][4 * q + 0] = v.x;
-          xv[mt][4 * q + 1] = v.y;
-          xv[mt][4 * q + 2] = v.z;
-          xv[mt][4 * q + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) xv[mt][q] = 0u;
-      }
-    }
-    uint32_t zsubA, zfmaA, zsubB, zfmaB;
-    float dA, dB;
-    zero_consts<kBF16>(f.sa, zsubA, zfmaA, dA);
-    zero_consts<kBF16>(f.sb, zsubB, zfmaB, dB);
-    float gacc[MT][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) gacc[mt][i] = 0.0f;
-    const uint32_t wa[4] = {f.a.x, f.a.y, f.a.z, f.a.w};
-    const uint32_t wb[4] = {f.b.x, f.b.y, f.b.z, f.b.w};
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      uint32_t hA[4], hB[4];
-      dequant_word<kBF16>(wa[w], zsubA, zfmaA, hA);
-      dequant_word<kBF16>(wb[w], zsubB, zfmaB, hB);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const uint32_t x01 = xv[mt][4 * w], x23 = xv[mt][4 * w + 1];
-        const uint32_t x45 = xv[mt][4 * w + 2], x67 = xv[mt][4 * w + 3];
-        const uint32_t p0 = prmt(x01, x45, 0x5410u), p1 = prmt(x01, x45, 0x7632u);
-        const uint32_t p2 = prmt(x23, x67, 0x5410u), p3 = prmt(x23, x67, 0x7632u);
-        mma_16816(gacc[mt], hA[0], hB[0], hA[1], hB[1], p0, p1, kBF16);
-        mma_16816(gacc[mt], hA[2], hB[2], hA[3], hB[3], p2, p3, kBF16);
-      }
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      acc[mt][0] = fmaf(gacc[mt][0], dA, acc[mt][0]);
-      acc[mt][1] = fmaf(gacc[mt][1], dA, acc[mt][1]);
-      acc[mt][2] = fmaf(gacc[mt][2], dB, acc[mt][2]);
-      acc[mt][3] = fmaf(gacc[mt][3], dB, acc[mt][3]);
-    }
-  };
-
-  // software pipeline: up to three groups of codes in flight per warp
-  {
-    int g = gbeg;
-    WFrag f0 = {}, f1 = {};
-    if (g < gend) f0 = load(g);
-    if (g + 1 < gend) f1 = load(g + 1);
-    for (; g < gend; g += 2) {
-      WFrag n0 = {};
-      if (g + 2 < gend) n0 = load(g + 2);
-      compute(f0, g);
-      WFrag n1 = {};
-      if (g + 3 < gend) n1 = load(g + 3);
-      if (g + 1 < gend) compute(f1, g + 1);
-      f0 = n0;
-      f1 = n1;
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();
 
-  auto to_out = [](float v) -> uint16_t {
-    if (kBF16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
-    return __half_as_ushort(__float2half_rn(v));
-  };
-
-  if (splits == 1) {
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int t0 = 8 * mt + 2 * j, t1 = t0 + 1;
-      if (t0 < M) {
-        if (okA) Y[(size_t)t0 * N + rowA] = to_out(acc[mt][0]);
-        if (okB) Y[(size_t)t0 * N + rowB] = to_out(acc[mt][2]);
-      }
-      if (t1 < M) {
-        if (okA) Y[(size_t)t1 * N + rowA] = to_out(acc[mt][1]);
-        if (okB) Y[(size_t)t1 * N + rowB] = to_out(acc[mt][3]);
+  if (warp == kConsumerWarps) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      prefetch_tmap(&tm_w);
+      prefetch_tmap(&tm_x);
+      prefetch_tmap(&tm_s);
+      prefetch_tmap(&tm_z);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
+        mbar_wait(bar_empty + 8 * s, ph ^ 1);
+        const uint32_t st = sbase + s * C::STAGE;
+        const uint32_t fb = bar_full + 8 * s;
+        mbar_expect_tx(fb, C::STAGE);
+        tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+        tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
+        tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
+        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+        if (++s == C::NS) { s = 0; ph ^= 1; }
       }
     }
     return;
   }
 
-  // ---- split-K: stage this CTA's fp32 partial tile, reduce over the cluster ----
+  // ===================== consumers: warp w = group w of each stage =====================
+  const int r = lane / 4, j = lane % 4;
+  float acc[4][MT][4];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int t0 = 8 * mt + 2 * j;
-    part[t0][warp * 16 + r] = acc[mt][0];
-    part[t0 + 1][warp * 16 + r] = acc[mt][1];
-    part[t0][warp * 16 + r + 8] = acc[mt][2];
-    part[t0 + 1][warp * 16 + r + 8] = acc[mt][3];
-  }
-  cg::cluster_group cluster = cg::this_cluster();
-  cluster.sync();
-  if (cluster.block_rank() == 0) {
-    const int nblk = blockIdx.y * kRowsPerCta;
-    for (int idx = threadIdx.x; idx < M * kRowsPerCta; idx += kThreads) {
-      const int t = idx / kRowsPerCta, row = idx % kRowsPerCta;
-      float s = 0.0f;
-      for (int rk = 0; rk < splits; ++rk) {
-        const float* peer = cluster.map_shared_rank(&part[0][0], rk);
-        s += peer[t * kRowsPerCta + row];
+  for (int rt = 0; rt < 4; ++rt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
+
+  int s = 0;
+  uint32_t ph = 0;
+  int seg_begin = u0;
+  for (int u = u0; u < u1; ++u) {
+    const int rb = u / wk.upb;
+    mbar_wait(bar_full + 8 * s, ph);
+    const uint32_t st = sbase + s * C::STAGE;
+
+    // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
+    uint32_t xb[MT][4][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int t = r + 8 * mt;
+      const int R = (warp * C::MPAD + t) * 2 + (j >> 1);  // 128-byte row in the swizzled box
+      const uint32_t rowaddr = st + C::CODES + R * 128;
+      uint32_t xv[16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 v = lds128(rowaddr + ((((j & 1) * 4 + i) ^ (R & 7)) << 4));
+        xv[4 * i] = v.x; xv[4 * i + 1] = v.y; xv[4 * i + 2] = v.z; xv[4 * i + 3] = v.w;
       }
-      if (nblk + row < N) Y[(size_t)t * N + nblk + row] = to_out(s);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        xb[mt][w][0] = prmt(xv[4 * w], xv[4 * w + 2], 0x5410u);      // (x0, x4)
+        xb[mt][w][1] = prmt(xv[4 * w], xv[4 * w + 2], 0x7632u);      // (x1, x5)
+        xb[mt][w][2] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x5410u);  // (x2, x6)
+        xb[mt][w][3] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x7632u);  // (x3, x7)
+      }
     }
+    const uint32_t cbase = st + warp * (BN * 64);
+    const uint32_t sbase_s = st + C::CODES + C::XB + warp * (BN * 2);
+    const uint32_t sbase_z = sbase_s + C::SZ;
+#pragma unroll
+    for (int rt = 0; rt < 4; ++rt) {
+      const int ra = rt * 16 + r, rbb = ra + 8;
+      const uint4 ca = lds128(cbase + ra * 64 + j * 16);
+      const uint4 cb = lds128(cbase + rbb * 64 + j * 16);
+      const float dA = __half2float(__ushort_as_half(lds16(sbase_s + ra * 2)));
+      const float dB = __half2float(__ushort_as_half(lds16(sbase_s + rbb * 2)));
+      uint32_t zsA, zfA, zsB, zfB;
+      zero_consts<kBF16>(lds16(sbase_z + ra * 2), zsA, zfA);
+      zero_consts<kBF16>(lds16(sbase_z + rbb * 2), zsB, zfB);
+      float g[MT][2][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { g[mt][0][i] = 0.0f; g[mt][1][i] = 0.0f; }
+      const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
+      const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t hA[4], hB[4];
+        dequant_word<kBF16>(wa[w], zsA, zfA, hA);
+        dequant_word<kBF16>(wb[w], zsB, zfB, hB);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma_16816(g[mt][0], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+          mma_16816(g[mt][1], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        acc[rt][mt][0] = fmaf(g[mt][0][0] + g[mt][1][0], dA, acc[rt][mt][0]);
+        acc[rt][mt][1] = fmaf(g[mt][0][1] + g[mt][1][1], dA, acc[rt][mt][1]);
+        acc[rt][mt][2] = fmaf(g[mt][0][2] + g[mt][1][2], dB, acc[rt][mt][2]);
+        acc[rt][mt][3] = fmaf(g[mt][0][3] + g[mt][1][3], dB, acc[rt][mt][3]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+    if (++s == C::NS) { s = 0; ph ^= 1; }
+
+    // ---- end of this CTA's segment of row block rb?
+    const bool seg_end = (u + 1 == u1) || ((u + 1) % wk.upb == 0);
+    if (!seg_end) continue;
+
+    // sum the 4 consumer warps through shared memory: warps 1..3 park, warp 0 adds
+    if (warp > 0) {
+      float* rw = red + (warp - 1) * C::MPAD * BN;
+#pragma unroll
+      for (int rt = 0; rt < 4; ++rt)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
+          rw[t0 * BN + ra] = acc[rt][mt][0];
+          rw[(t0 + 1) * BN + ra] = acc[rt][mt][1];
+          rw[t0 * BN + ra + 8] = acc[rt][mt][2];
+          rw[(t0 + 1) * BN + ra + 8] = acc[rt][mt][3];
+        }
+    }
+    consumer_sync();
+    if (warp == 0) {
+#pragma unroll
+      for (int rt = 0; rt < 4; ++rt)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
+          float v[4] = {acc[rt][mt][0], acc[rt][mt][1], acc[rt][mt][2], acc[rt][mt][3]};
+#pragma unroll
+          for (int w = 0; w < kConsumerWarps - 1; ++w) {
+            const float* rw = red + w * C::MPAD * BN;
+            v[0] += rw[t0 * BN + ra];
+            v[1] += rw[(t0 + 1) * BN + ra];
+            v[2] += rw[t0 * BN + ra + 8];
+            v[3] += rw[(t0 + 1) * BN + ra + 8];
+          }
+          // park the CTA's total in warp 1's slot for the coalesced write-out below
+          float* tot = red;
+          tot[t0 * BN + ra] = v[0];
+          tot[(t0 + 1) * BN + ra] = v[1];
+          tot[t0 * BN + ra + 8] = v[2];
+          tot[(t0 + 1) * BN + ra + 8] = v[3];
+        }
+    }
+    consumer_sync();
+#pragma unroll
+    for (int rt = 0; rt < 4; ++rt)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
+
+    const int n0 = rb * BN;
+    const bool full = (seg_begin == rb * wk.upb) && (u + 1 == (rb + 1) * wk.upb);
+    auto to_out = [](float v) -> uint16_t {
+      if (kBF16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+      return __half_as_ushort(__float2half_rn(v));
+    };
+    if (full) {
+      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) {
+        const int t = idx / BN, row = idx % BN;
+        if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(red[t * BN + row]);
+      }
+    } else {
+      // stream-K fixup: park the partial, the last contributor sums them in CTA order
+      const int e = (seg_begin == u0) ? 0 : 1;
+      float* slot = partials + ((size_t)c * 2 + e) * (16 * BN);
+      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) slot[idx] = red[idx];
+      __threadfence();
+      consumer_sync();
+      if (threadIdx.x == 0) {
+        const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
+        const int prev = atomicAdd(counters + rb, 1);
+        *flag = (prev == c1 - c0) ? 1 : 0;
+      }
+      consumer_sync();
+      if (*flag) {
+        __threadfence();
+        const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
+        for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) {
+          float v = 0.0f;
+          for (int cc = c0; cc <= c1; ++cc) {
+            const int ee = (wk.start(cc) / wk.upb == rb) ? 0 : 1;
+            v += __ldcg(partials + ((size_t)cc * 2 + ee) * (16 * BN) + idx);
+          }
+          const int t = idx / BN, row = idx % BN;
+          if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(v);
+        }
+        if (threadIdx.x == 0) counters[rb] = 0;  // leave the workspace zeroed
+      }
+    }
+    consumer_sync();  // red[] is reused by the next segment
+    seg_begin = u + 1;
   }
-  cluster.sync();
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
+            const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  auto fn = get_encode();
+  if (!fn) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  return fn(map, dt, rank, const_cast<void*>(base), d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int MT, bool kBF16>
-cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales,
-                     const uint16_t* zeros, void* Y, int M, int N, int K, const DecodePlan& p,
-                     cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)p.splits, (unsigned)p.row_blocks, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)p.splits;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16>, (const uint16_t*)X, Wq, scales, zeros,
-                            (uint16_t*)Y, M, N, K, p.splits);
+int ctas_per_sm() {
+  static int cached = -1;
+  if (cached < 0) {
+    int n = 0;
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<MT>::SMEM_ALLOC);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16>, kThreads,
+                                                      Cfg<MT>::SMEM_ALLOC) != cudaSuccess || n < 1)
+      n = 1;
+    cached = std::min(n, kMaxCtasPerSm);
+  }
+  return cached;
+}
+
+template <int MT, bool kBF16>
+cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                     void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
+  using C = Cfg<MT>;
+  const int G = K / kGroup;
+  CUtensorMap tw, tx, ts, tz;
+  {
+    const uint64_t d[3] = {64, (uint64_t)N, (uint64_t)G};
+    const uint64_t s[2] = {(uint64_t)K / 2, 64};
+    const uint32_t b[3] = {64, BN, GPS};
+    if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, Wq, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      *why = "tensor map (codes)";
+      return cudaErrorInvalidValue;
+    }
+  }
+  {
+    const uint64_t d[4] = {64, 2, (uint64_t)M, (uint64_t)G};
+    const uint64_t s[3] = {128, (uint64_t)K * 2, 256};
+    const uint32_t b[4] = {64, 2, (uint32_t)C::MPAD, GPS};
+    if (!encode(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, X, d, s, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      *why = "tensor map (X)";
+      return cudaErrorInvalidValue;
+    }
+  }
+  {
+    const uint64_t d[2] = {(uint64_t)N, (uint64_t)G};
+    const uint64_t s[1] = {(uint64_t)N * 2};
+    const uint32_t b[2] = {BN, GPS};
+    if (!encode(&ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, scales, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, zeros, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      *why = "tensor map (scales/zeros)";
+      return cudaErrorInvalidValue;
+    }
+  }
+  const int RB = (N + BN - 1) / BN;
+  Work wk;
+  wk.upb = (G + GPS - 1) / GPS;
+  wk.units = RB * wk.upb;
+  const int P = std::min(wk.units, num_sms() * ctas_per_sm<MT, kBF16>());
+  wk.cta_q = wk.units / P;
+  wk.cta_r = wk.units % P;
+  int* counters = reinterpret_cast<int*>(ws);
+  float* partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + decode_counter_bytes(N));
+  decode_kernel<MT, kBF16><<<P, kThreads, C::SMEM_ALLOC, st>>>(tw, tx, ts, tz, (uint16_t*)Y, counters,
+                                                               partials, M, N, wk);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-DecodePlan plan_decode(int64_t M, int64_t N, int64_t K) {
-  (void)M;
-  DecodePlan p;
-  p.rows_per_cta = kRowsPerCta;
-  p.row_blocks = (int)((N + kRowsPerCta - 1) / kRowsPerCta);
-  const int G = (int)(K / kGroup);
-  // CTAs resident at once (4 warps each, ~4 per SM); split K over a cluster only as
-  // far as the whole grid still fits in one wave, and keep >= 4 groups per CTA.
-  const int slots = 4 * num_sms();
-  int s = 1;
-  while (s * 2 <= 8 && (int64_t)p.row_blocks * s * 2 <= slots && G / (s * 2) >= 4) s *= 2;
-  p.splits = s;
-  return p;
+size_t decode_counter_bytes(int64_t N) {
+  const int64_t RB = (N + BN - 1) / BN;
+  return (size_t)((RB * 4 + 255) / 256 * 256);
+}
+
+size_t decode_workspace_bytes(int64_t N) {
+  return decode_counter_bytes(N) + (size_t)num_sms() * kMaxCtasPerSm * 2 * 16 * BN * sizeof(float);
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K,
-                          const DecodePlan& plan, cudaStream_t st) {
+                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
+                          cudaStream_t st, const char** why) {
   const bool bf16 = x_dtype == SQ_BF16;
   if (M <= 8)
-    return bf16 ? launch_t<1, true>(X, Wq, scales, zeros, Y, M, N, K, plan, st)
-                : launch_t<1, false>(X, Wq, scales, zeros, Y, M, N, K, plan, st);
-  return bf16 ? launch_t<2, true>(X, Wq, scales, zeros, Y, M, N, K, plan, st)
-              : launch_t<2, false>(X, Wq, scales, zeros, Y, M, N, K, plan, st);
+    return bf16 ? launch_t<1, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+                : launch_t<1, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+  return bf16 ? launch_t<2, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+              : launch_t<2, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
 }
 
 }  // namespace sq

@@ -2,6 +2,7 @@
 // Host-only code; every kernel launch is asynchronous on the caller's stream.
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -125,8 +126,9 @@ sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s,
 
 size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group) {
   (void)group;
-  if (M <= kDecodeMaxM) return 0;
-  return prefill_workspace_bytes(M, N, K);
+  if (N <= 0 || K <= 0 || M < 0) return 0;
+  // enough for either path, so one buffer serves SQ_PATH_AUTO and the explicit paths
+  return std::max(decode_workspace_bytes(N), prefill_workspace_bytes(M, N, K));
 }
 
 sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
@@ -148,8 +150,13 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
   if (path == SQ_PATH_AUTO) path = (M <= kDecodeMaxM) ? SQ_PATH_DECODE : SQ_PATH_PREFILL;
   if (path == SQ_PATH_DECODE) {
     if (M > kDecodeMaxM) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: decode path needs M <= %d", kDecodeMaxM);
-    DecodePlan p = plan_decode(M, N, K);
-    return cuda_status(launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, p, st), "decode");
+    const size_t need = decode_workspace_bytes(N);
+    if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
+      return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: decode needs %zu workspace bytes (16-byte aligned)", need);
+    const char* why = nullptr;
+    cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why);
+    if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
+    return cuda_status(e, "decode");
   }
   if (path == SQ_PATH_PREFILL) {
     const size_t need = prefill_workspace_bytes(M, N, K);

@@ -19,15 +19,11 @@ cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t 
                             uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
                             cudaStream_t st);
 
-struct DecodePlan {
-  int rows_per_cta;   // 64
-  int splits;         // cluster size along K (1..8)
-  int row_blocks;
-};
-DecodePlan plan_decode(int64_t M, int64_t N, int64_t K);
+size_t decode_counter_bytes(int64_t N);
+size_t decode_workspace_bytes(int64_t N);
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K,
-                          const DecodePlan& plan, cudaStream_t st);
+                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
+                          cudaStream_t st, const char** why);
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,

@@ -171,6 +171,20 @@ def w4a16_gemm_workspace_bytes(M: int, N: int, K: int, group: int = GROUP) -> in
     return int(_load().sq_w4a16_gemm_workspace_bytes(M, N, K, group))
 
 
+_WS: dict = {}
+
+
+def default_workspace(device, nbytes: int) -> torch.Tensor:
+    """A zero-filled per-device workspace, grown on demand (plumbing only: one
+    workspace per device means GEMMs on one device must share a stream)."""
+    key = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
 def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = None,
                workspace: torch.Tensor | None = None, path: int = SQ_PATH_AUTO,
                stream=None) -> torch.Tensor:
@@ -181,6 +195,10 @@ def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = N
         raise ValueError(f"K mismatch: X has {K}, weight has {q.K}")
     if out is None:
         out = torch.empty((M, q.N), dtype=X.dtype, device=X.device)
+    if workspace is None:
+        need = w4a16_gemm_workspace_bytes(M, q.N, K, q.group)
+        if need:
+            workspace = default_workspace(X.device, need)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(_load().sq_w4a16_gemm_path(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
                                       _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes, int(path),

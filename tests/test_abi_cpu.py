@@ -93,5 +93,13 @@ def test_smooth_argument_errors(L):
 
 
 def test_workspace_query(L):
-    assert L.sq_w4a16_gemm_workspace_bytes(1, 8192, 8192, 128) == 0
+    # decode: per-row-block counters + 2 fp32 partial tiles per resident CTA
+    small = L.sq_w4a16_gemm_workspace_bytes(1, 8192, 8192, 128)
+    assert small >= 8192 // 64 * 4
+    assert L.sq_w4a16_gemm_workspace_bytes(1, 44032, 8192, 128) >= small
     assert L.sq_w4a16_gemm_workspace_bytes(2048, 8192, 8192, 128) >= 0
+    assert L.sq_w4a16_gemm_workspace_bytes(1, 0, 8192, 128) == 0
+
+
+def test_decode_requires_workspace(L):
+    assert _gemm(L, M=4, path=1) == sq.SQ_ERR_WORKSPACE
