@@ -241,6 +241,10 @@ def main():
 
     # ---------------- decode stack (the headline)
     st = stack.build_stack(model, a.layers, rank, world, dev, group=pg)
+    torch.cuda.synchronize()
+    # inference: the quantized weights are resident and never written while the GEMMs
+    # run, so the decode kernel may stream them ahead of the previous kernel (PDL)
+    sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
     bufs = [stack.make_buffers(st, M, dev) for M in ms]
     if world > 1:
         t = torch.ones(1, device=dev)
@@ -402,6 +406,7 @@ def main():
 
     # ---------------- load-time smoothing + quantization (a1-a4)
     quant = None
+    sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 0)  # quantize writes the weights GEMMs read
     if not a.skip_quant:
         Ws, ams = [], []
         for si, sh in enumerate(st.shards):
@@ -454,7 +459,8 @@ def main():
                        "parallelism": f"tp{world}" if world > 1 else "none",
                        "weights_bytes_per_step_all_ranks": bytes_all,
                        "l2": "no flush: every pass streams the stack's weights (GBs) > 126 MB L2",
-                       "cuda_graph": used_graph},
+                       "cuda_graph": used_graph, "pdl": sq.get_option(sq.SQ_OPT_PDL),
+                       "weights_static": sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC)},
             "gpu_launches": launches_per_step * a.steps,
             "clocks": clocks,
             "roofline": roofline,

@@ -65,6 +65,16 @@ enum {
 };
 enum { SQ_F16 = 0, SQ_BF16 = 1 };
 enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
+/* Process-wide launch options (sq_set_option):
+ *  SQ_OPT_PDL (default 1): launch the GEMM kernels with programmatic dependent
+ *    launch, so a kernel's prologue overlaps the previous kernel's tail; every
+ *    read of X and every global write still waits for the previous kernel
+ *    (griddepcontrol.wait), so results are unchanged.
+ *  SQ_OPT_WEIGHTS_STATIC (default 0): the caller promises that Wq/scales/zeros
+ *    are not written by the kernels that immediately precede a GEMM on its
+ *    stream (true for inference with resident weights).  The decode kernel then
+ *    streams its first weight stages BEFORE waiting on the previous kernel. */
+enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2 };
 
 /* Library version (major*10000 + minor*100 + patch). */
 SQ_API int sq_version(void);
@@ -74,6 +84,10 @@ SQ_API const char* sq_status_string(sq_status st);
 SQ_API const char* sq_last_error(void);
 /* Largest M served by the decode path under SQ_PATH_AUTO (M_dec). */
 SQ_API int sq_decode_max_m(void);
+/* Set / read a launch option (SQ_OPT_*); returns SQ_ERR_UNSUPPORTED for an
+ * unknown option.  sq_get_option returns -1 for an unknown option. */
+SQ_API sq_status sq_set_option(int option, int value);
+SQ_API int sq_get_option(int option);
 
 /*
  * Calibration statistic of Eq. 6: act_max[k] = max_t |X[t][k]| over the T rows

@@ -129,6 +129,24 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a
   }
 }
 
+__device__ __forceinline__ void mma_16816_zc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t a3, uint32_t b0, uint32_t b1, bool bf16) {
+  const float z = 0.0f;
+  if (bf16) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%10,%10,%10,%10};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(z));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%10,%10,%10,%10};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(z));
+  }
+}
+
 __device__ __forceinline__ uint32_t hsub2_u(uint32_t a, uint32_t b, bool bf16) {
   if (bf16) {
     __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a),
@@ -167,39 +185,41 @@ template <bool kBF16>
 __device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint32_t& zfma) {
   const uint32_t z = (uint32_t)__half2int_rn(__ushort_as_half(zbits));
   if (!kBF16) {
-    const uint32_t c1 = 0x6400u + z;          // fp16(1024 + Z): ulp of 1024 is 1
-    const uint32_t c2 = 0xD400u + (z << 4);   // fp16(-(64 + Z)): ulp of 64 is 1/16
-    zsub = c1 | (c1 << 16);
-    zfma = c2 | (c2 << 16);
+    zsub = z * 0x00010001u + 0x64006400u;         // fp16x2(1024 + Z): ulp of 1024 is 1
+    zfma = z * 0x00100010u + 0xD400D400u;         // fp16x2(-(64 + Z)): ulp of 64 is 1/16
   } else {
-    const uint32_t c1 = 0x4300u + z;          // bf16(128 + Z): ulp of 128 is 1
-    zsub = c1 | (c1 << 16);
+    zsub = z * 0x00010001u + 0x43004300u;         // bf16x2(128 + Z): ulp of 128 is 1
     zfma = 0;
   }
 }
 
 struct Work {
   int units, upb, cta_q, cta_r;  // total units, units per row block, units per CTA (q, remainder)
-  __device__ int start(int c) const { return c * cta_q + min(c, cta_r); }
-  __device__ int cta_of(int u) const {
+  __device__ __forceinline__ int start(int c) const { return c * cta_q + min(c, cta_r); }
+  __device__ __forceinline__ int cta_of(int u) const {
     const int big = (cta_q + 1) * cta_r;
     return u < big ? u / (cta_q + 1) : cta_r + (u - big) / cta_q;
   }
 };
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 template <int MT, bool kBF16>
 __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
-              int M, int N, Work wk) {
+              int M, int N, Work wk, int early_weights) {
   using C = Cfg<MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + C::OFF_BAR;
   const uint32_t bar_empty = bar_full + 8 * C::NS;
-  volatile int* flag = reinterpret_cast<volatile int*>(smem + C::OFF_FLAG);
+  int* flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
   float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -214,6 +234,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // the next kernel in the stream may start its prologue as our CTAs retire
+  pdl_launch_dependents();
 
   if (warp == kConsumerWarps) {
     // ===================== TMA producer =====================
@@ -222,19 +244,42 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       prefetch_tmap(&tm_x);
       prefetch_tmap(&tm_s);
       prefetch_tmap(&tm_z);
+      // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
+      // declared them static: stream the first stages before waiting on it.
+      int pre = 0;
+      if (early_weights) {
+        int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
+        for (; pre < C::NS && u0 + pre < u1; ++pre) {
+          const uint32_t st = sbase + pre * C::STAGE;
+          const uint32_t fb = bar_full + 8 * pre;
+          mbar_expect_tx(fb, C::STAGE);
+          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+          tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
+          tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+          g0 += GPS;
+          if (g0 >= wk.upb * GPS) { g0 = 0; ++rb; }
+        }
+      }
+      pdl_wait();  // X (and everything after) may be the previous kernel's output
+      int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
       int s = 0;
       uint32_t ph = 0;
-      for (int u = u0; u < u1; ++u) {
-        const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
-        mbar_wait(bar_empty + 8 * s, ph ^ 1);
+      for (int i = 0; u0 + i < u1; ++i) {
         const uint32_t st = sbase + s * C::STAGE;
         const uint32_t fb = bar_full + 8 * s;
-        mbar_expect_tx(fb, C::STAGE);
-        tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
-        tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
-        tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
-        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+        if (i < pre) {
+          tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
+        } else {
+          mbar_wait(bar_empty + 8 * s, ph ^ 1);
+          mbar_expect_tx(fb, C::STAGE);
+          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+          tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
+          tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
+          tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+        }
         if (++s == C::NS) { s = 0; ph ^= 1; }
+        g0 += GPS;
+        if (g0 >= wk.upb * GPS) { g0 = 0; ++rb; }
       }
     }
     return;
@@ -252,9 +297,12 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   int s = 0;
   uint32_t ph = 0;
-  int seg_begin = u0;
+  int rb = u0 / wk.upb;            // current row block
+  int pos = u0 - rb * wk.upb;      // unit index inside the row block
+  int seg_begin_pos = pos;
+  bool first_seg = true;
+  bool waited = false;
   for (int u = u0; u < u1; ++u) {
-    const int rb = u / wk.upb;
     mbar_wait(bar_full + 8 * s, ph);
     const uint32_t st = sbase + s * C::STAGE;
 
@@ -262,8 +310,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     uint32_t xb[MT][4][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
-      const int t = r + 8 * mt;
-      const int R = (warp * C::MPAD + t) * 2 + (j >> 1);  // 128-byte row in the swizzled box
+      const int R = (warp * C::MPAD + r + 8 * mt) * 2 + (j >> 1);  // 128-byte row of the swizzled box
       const uint32_t rowaddr = st + C::CODES + R * 128;
       uint32_t xv[16];
 #pragma unroll
@@ -279,26 +326,21 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         xb[mt][w][3] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x7632u);  // (x3, x7)
       }
     }
-    const uint32_t cbase = st + warp * (BN * 64);
-    const uint32_t sbase_s = st + C::CODES + C::XB + warp * (BN * 2);
-    const uint32_t sbase_z = sbase_s + C::SZ;
+    const uint32_t cbase = st + warp * (BN * 64) + r * 64 + j * 16;
+    const uint32_t sbs = st + C::CODES + C::XB + warp * (BN * 2) + r * 2;
+    const uint32_t sbz = sbs + C::SZ;
 #pragma unroll
     for (int rt = 0; rt < 4; ++rt) {
-      const int ra = rt * 16 + r, rbb = ra + 8;
-      const uint4 ca = lds128(cbase + ra * 64 + j * 16);
-      const uint4 cb = lds128(cbase + rbb * 64 + j * 16);
-      const float dA = __half2float(__ushort_as_half(lds16(sbase_s + ra * 2)));
-      const float dB = __half2float(__ushort_as_half(lds16(sbase_s + rbb * 2)));
+      const uint4 ca = lds128(cbase + rt * 16 * 64);
+      const uint4 cb = lds128(cbase + (rt * 16 + 8) * 64);
+      const float dA = __half2float(__ushort_as_half(lds16(sbs + rt * 32)));
+      const float dB = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
       uint32_t zsA, zfA, zsB, zfB;
-      zero_consts<kBF16>(lds16(sbase_z + ra * 2), zsA, zfA);
-      zero_consts<kBF16>(lds16(sbase_z + rbb * 2), zsB, zfB);
-      float g[MT][2][4];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { g[mt][0][i] = 0.0f; g[mt][1][i] = 0.0f; }
+      zero_consts<kBF16>(lds16(sbz + rt * 32), zsA, zfA);
+      zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB, zfB);
       const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
       const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+      float g[MT][4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t hA[4], hB[4];
@@ -306,16 +348,20 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         dequant_word<kBF16>(wb[w], zsB, zfB, hB);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          mma_16816(g[mt][0], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
-          mma_16816(g[mt][1], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
+          if (w == 0) {
+            mma_16816_zc(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+          } else {
+            mma_16816(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+          }
+          mma_16816(g[mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
         }
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        acc[rt][mt][0] = fmaf(g[mt][0][0] + g[mt][1][0], dA, acc[rt][mt][0]);
-        acc[rt][mt][1] = fmaf(g[mt][0][1] + g[mt][1][1], dA, acc[rt][mt][1]);
-        acc[rt][mt][2] = fmaf(g[mt][0][2] + g[mt][1][2], dB, acc[rt][mt][2]);
-        acc[rt][mt][3] = fmaf(g[mt][0][3] + g[mt][1][3], dB, acc[rt][mt][3]);
+        acc[rt][mt][0] = fmaf(g[mt][0], dA, acc[rt][mt][0]);
+        acc[rt][mt][1] = fmaf(g[mt][1], dA, acc[rt][mt][1]);
+        acc[rt][mt][2] = fmaf(g[mt][2], dB, acc[rt][mt][2]);
+        acc[rt][mt][3] = fmaf(g[mt][3], dB, acc[rt][mt][3]);
       }
     }
     __syncwarp();
@@ -323,9 +369,14 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     if (++s == C::NS) { s = 0; ph ^= 1; }
 
     // ---- end of this CTA's segment of row block rb?
-    const bool seg_end = (u + 1 == u1) || ((u + 1) % wk.upb == 0);
-    if (!seg_end) continue;
+    ++pos;
+    const bool rb_done = pos == wk.upb;
+    if (!rb_done && u + 1 != u1) continue;
 
+    if (!waited) {  // global writes below must follow the previous kernel (PDL)
+      pdl_wait();
+      waited = true;
+    }
     // sum the 4 consumer warps through shared memory: warps 1..3 park, warp 0 adds
     if (warp > 0) {
       float* rw = red + (warp - 1) * C::MPAD * BN;
@@ -356,12 +407,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
             v[2] += rw[t0 * BN + ra + 8];
             v[3] += rw[(t0 + 1) * BN + ra + 8];
           }
-          // park the CTA's total in warp 1's slot for the coalesced write-out below
-          float* tot = red;
-          tot[t0 * BN + ra] = v[0];
-          tot[(t0 + 1) * BN + ra] = v[1];
-          tot[t0 * BN + ra + 8] = v[2];
-          tot[(t0 + 1) * BN + ra + 8] = v[3];
+          red[t0 * BN + ra] = v[0];  // total parked in slot 0 (each lane owns its entries)
+          red[(t0 + 1) * BN + ra] = v[1];
+          red[t0 * BN + ra + 8] = v[2];
+          red[(t0 + 1) * BN + ra + 8] = v[3];
         }
     }
     consumer_sync();
@@ -373,7 +422,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
 
     const int n0 = rb * BN;
-    const bool full = (seg_begin == rb * wk.upb) && (u + 1 == (rb + 1) * wk.upb);
+    const bool full = (seg_begin_pos == 0) && rb_done;
     auto to_out = [](float v) -> uint16_t {
       if (kBF16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
       return __half_as_ushort(__float2half_rn(v));
@@ -384,26 +433,36 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(red[t * BN + row]);
       }
     } else {
-      // stream-K fixup: park the partial, the last contributor sums them in CTA order
-      const int e = (seg_begin == u0) ? 0 : 1;
+      // stream-K fixup: park the partial; the last contributor sums them in CTA order
+      const int e = first_seg ? 0 : 1;
       float* slot = partials + ((size_t)c * 2 + e) * (16 * BN);
-      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) slot[idx] = red[idx];
-      __threadfence();
+      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) __stcg(slot + idx, red[idx]);
       consumer_sync();
+      const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
       if (threadIdx.x == 0) {
-        const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
+        __threadfence();
         const int prev = atomicAdd(counters + rb, 1);
+        __threadfence();
         *flag = (prev == c1 - c0) ? 1 : 0;
       }
       consumer_sync();
       if (*flag) {
-        __threadfence();
-        const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
         for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) {
+          float part[8];
           float v = 0.0f;
-          for (int cc = c0; cc <= c1; ++cc) {
-            const int ee = (wk.start(cc) / wk.upb == rb) ? 0 : 1;
-            v += __ldcg(partials + ((size_t)cc * 2 + ee) * (16 * BN) + idx);
+          int cc = c0;
+          while (cc <= c1) {  // batch the L2 reads, add in fixed CTA order
+            const int nb = min(8, c1 - cc + 1);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < nb) {
+                const int ee = (wk.start(cc + q) / wk.upb == rb) ? 0 : 1;
+                part[q] = __ldcg(partials + ((size_t)(cc + q) * 2 + ee) * (16 * BN) + idx);
+              }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < nb) v += part[q];
+            cc += nb;
           }
           const int t = idx / BN, row = idx % BN;
           if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(v);
@@ -411,8 +470,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         if (threadIdx.x == 0) counters[rb] = 0;  // leave the workspace zeroed
       }
     }
-    consumer_sync();  // red[] is reused by the next segment
-    seg_begin = u + 1;
+    consumer_sync();  // red[] and flag are reused by the next segment
+    first_seg = false;
+    if (rb_done) { ++rb; pos = 0; }
+    seg_begin_pos = pos;
   }
 }
 
@@ -500,9 +561,19 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   wk.cta_r = wk.units % P;
   int* counters = reinterpret_cast<int*>(ws);
   float* partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + decode_counter_bytes(N));
-  decode_kernel<MT, kBF16><<<P, kThreads, C::SMEM_ALLOC, st>>>(tw, tx, ts, tz, (uint16_t*)Y, counters,
-                                                               partials, M, N, wk);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)P, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_ALLOC;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = option(SQ_OPT_PDL) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16>, tw, tx, ts, tz, (uint16_t*)Y, counters,
+                            partials, M, N, wk, early);
 }
 
 }  // namespace

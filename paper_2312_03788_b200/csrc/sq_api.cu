@@ -46,6 +46,17 @@ int num_sms() {
 
 constexpr int kDecodeMaxM = 16;
 
+static int g_opt_pdl = 1;
+static int g_opt_weights_static = 0;
+
+int option(int opt) {
+  switch (opt) {
+    case SQ_OPT_PDL: return g_opt_pdl;
+    case SQ_OPT_WEIGHTS_STATIC: return g_opt_weights_static;
+    default: return -1;
+  }
+}
+
 }  // namespace sq
 
 using namespace sq;
@@ -70,6 +81,16 @@ const char* sq_status_string(sq_status st) {
 const char* sq_last_error(void) { return g_last_error.c_str(); }
 
 int sq_decode_max_m(void) { return kDecodeMaxM; }
+
+sq_status sq_set_option(int opt, int value) {
+  switch (opt) {
+    case SQ_OPT_PDL: g_opt_pdl = value ? 1 : 0; return SQ_OK;
+    case SQ_OPT_WEIGHTS_STATIC: g_opt_weights_static = value ? 1 : 0; return SQ_OK;
+    default: return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: unknown option %d", opt);
+  }
+}
+
+int sq_get_option(int opt) { return option(opt); }
 
 sq_status sq_act_absmax(const void* X, int x_dtype, int64_t T, int64_t K, float* act_max,
                         int accumulate, void* stream) {

@@ -31,6 +31,7 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
                            void* workspace, size_t ws_bytes, cudaStream_t st, const char** why);
 
 int num_sms();
+int option(int opt);
 
 // ---- small device helpers ----
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t and_mask, uint32_t or_mask) {

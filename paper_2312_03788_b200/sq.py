@@ -26,6 +26,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libsq.so")
 SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
 SQ_F16, SQ_BF16 = 0, 1
 SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
+SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC = 1, 2
 GROUP = 128
 
 _lib = None
@@ -51,6 +52,8 @@ def _load():
         "sq_status_string": (c.c_char_p, [i32]),
         "sq_last_error": (c.c_char_p, []),
         "sq_decode_max_m": (i32, []),
+        "sq_set_option": (i32, [i32, i32]),
+        "sq_get_option": (i32, [i32]),
         "sq_act_absmax": (i32, [vp, i32, i64, i64, vp, i32, vp]),
         "sq_smooth_scales": (i32, [vp, i32, i64, i64, vp, f64, f64, vp, vp]),
         "sq_quantize_pack_groupwise": (i32, [vp, i32, vp, i64, i64, i32, vp, vp, vp, vp, vp]),
@@ -67,7 +70,8 @@ def _load():
 
 
 EXPORTED = (
-    "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_act_absmax",
+    "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_set_option",
+    "sq_get_option", "sq_act_absmax",
     "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
     "sq_w4a16_gemm", "sq_w4a16_gemm_path",
 )
@@ -114,6 +118,15 @@ def version() -> int:
 
 def decode_max_m() -> int:
     return _load().sq_decode_max_m()
+
+
+def set_option(opt: int, value: int) -> None:
+    """Process-wide launch option (SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC; include/libsq.h)."""
+    _check(_load().sq_set_option(int(opt), int(value)))
+
+
+def get_option(opt: int) -> int:
+    return int(_load().sq_get_option(int(opt)))
 
 
 def act_absmax(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,

@@ -227,3 +227,35 @@ def test_gemm_m_zero_noop():
     x = torch.zeros((0, 256), dtype=torch.float16, device=DEV)
     y = sq.w4a16_gemm(x, q)
     assert y.shape == (0, 128)
+
+
+@pytest.mark.parametrize("pdl,static", [(0, 0), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M", [1, 16])
+def test_gemm_chain_launch_options(pdl, static, M):
+    """A dependent chain y_{i+1} = y_i · Ŵ_i^T (each GEMM reads the previous one's
+    output) under programmatic dependent launch and early weight streaming: the
+    kernels must still wait for their inputs (include/libsq.h SQ_OPT_*)."""
+    D = 512
+    Ws = [synth.weights(D, D, seed=300 + i) for i in range(4)]
+    refs = [oracle.quantize_pack(W, None) for W in Ws]
+    qs = [sq.quantize_pack_groupwise(_t(W)) for W in Ws]
+    torch.cuda.synchronize()  # weights static before the chain (SQ_OPT_WEIGHTS_STATIC contract)
+    X = (synth.activations(M, D, seed=9) * 0.05).astype(np.float16)
+    old = (sq.get_option(sq.SQ_OPT_PDL), sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC))
+    try:
+        sq.set_option(sq.SQ_OPT_PDL, pdl)
+        sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, static)
+        y = torch.from_numpy(X).to(DEV)
+        for _ in range(3):
+            for q in qs:
+                y = sq.w4a16_gemm(y, q, path=sq.SQ_PATH_DECODE)
+        torch.cuda.synchronize()
+    finally:
+        sq.set_option(sq.SQ_OPT_PDL, old[0])
+        sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, old[1])
+    yr = X.copy()
+    for _ in range(3):
+        for r in refs:
+            yr = oracle.gemm(yr, r["Wq"], r["scales"], r["zeros"]).astype(np.float16)
+    yr = yr.astype(np.float64)
+    assert _rel_frob(y, yr) <= 1e-2
