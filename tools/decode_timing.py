@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--shapes", default="o,gate,gate_up,down")
     ap.add_argument("--m", default="1,16")
     ap.add_argument("--launches", type=int, default=64)
+    ap.add_argument("--tail", default="0")
     a = ap.parse_args()
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -32,7 +33,12 @@ def main():
         del W
         qs = [q0] + [sq.QuantizedLinear(q0.Wq.clone(), q0.scales.clone(), q0.zeros.clone(), N, K)
                      for _ in range(copies - 1)]
-        for M in [int(x) for x in a.m.split(",")]:
+        import ctypes
+        L = sq.lib()
+        L.sq_debug_set_decode_tail.argtypes = [ctypes.c_float]
+        sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
+        for M, tail in [(int(m), float(tf)) for m in a.m.split(",") for tf in a.tail.split(",")]:
+            L.sq_debug_set_decode_tail(tail)
             x = torch.randn(M, K, device=dev).half()
             y = torch.empty(M, N, device=dev, dtype=torch.half)
             ws = sq.default_workspace(dev, sq.w4a16_gemm_workspace_bytes(M, N, K))
@@ -53,7 +59,7 @@ def main():
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) * 1e-3 / (5 * a.launches)
             B = wb + 2 * M * K + 2 * M * N
-            print(json.dumps({"shape": name, "M": M, "us": t * 1e6, "GBs": B / t / 1e9,
+            print(json.dumps({"shape": name, "M": M, "tail": tail, "us": t * 1e6, "GBs": B / t / 1e9,
                               "frac": B / t / 1e9 / peak}), flush=True)
         del qs, q0
         torch.cuda.empty_cache()
