@@ -69,13 +69,18 @@ def load_peaks():
         return dict(FALLBACK_PEAKS), "fallback"
 
 
-def load_ncu_traffic(kernel_key: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+def load_ncu_traffic(kernel_key: str, bytes_per_launch: float):
+    """DRAM traffic per launch of the dominant kernel, from the committed ncu capture
+    (profiles/ncu_summary.json): the captured launch's dram read+write bytes over its
+    algorithmic bytes, applied to this run's average launch."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+            d = json.load(f)[kernel_key]
+        ratio = d["traffic_over_algorithmic"]
+        return {"per_launch": ratio * bytes_per_launch, "ratio_to_algorithmic": ratio,
+                "captured": {"what": d["what"], "dram_bytes": d["dram_bytes_per_launch"],
+                             "algorithmic_bytes": d["algorithmic_bytes"], "source": "profiles/" + d["report"]}}
     except Exception:
         return None
 
@@ -245,6 +250,7 @@ def main():
     # inference: the quantized weights are resident and never written while the GEMMs
     # run, so the decode kernel may stream them ahead of the previous kernel (PDL)
     sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
+    launch_opts = {"pdl": sq.get_option(sq.SQ_OPT_PDL), "weights_static": sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC)}
     bufs = [stack.make_buffers(st, M, dev) for M in ms]
     if world > 1:
         t = torch.ones(1, device=dev)
@@ -304,10 +310,10 @@ def main():
     dec_bytes_launch = bytes_rank / launches_per_step
     hbm_peak = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     achieved = dec_bytes_launch / dec_launch_s / 1e9
-    traffic = load_ncu_traffic("decode")
+    traffic = load_ncu_traffic("decode", dec_bytes_launch)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
-                "kernel": "sq::decode_kernel (mma.sync W4A16, cluster split-K)",
+                "kernel": "sq::decode_kernel (TMA-fed mma.sync W4A16, persistent stream-K)",
                 "peak_source": f"{peaks_src} hbm_gbs", "bytes_per_launch": dec_bytes_launch}
 
     # per-M breakdown (graph per M), for the report
@@ -397,7 +403,8 @@ def main():
         prefill = {"value": tf, "unit": "TFLOP/s", "M": M, "layers": len(pst.layers),
                    "ms_per_pass": tpre * 1e3,
                    "roofline": {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
-                                "frac": ach / tc_peak, "traffic": load_ncu_traffic("prefill"),
+                                "frac": ach / tc_peak,
+                                "traffic": load_ncu_traffic("prefill", stack.pass_bytes(pst, M) / n_l),
                                 "kernel": "sq::prefill_kernel (TMA + tcgen05.mma, A in TMEM)",
                                 "peak_source": f"{peaks_src} bf16_tflops (fp16 dense = bf16 dense)",
                                 "flops_per_launch": flops_rank / n_l}}
@@ -459,8 +466,7 @@ def main():
                        "parallelism": f"tp{world}" if world > 1 else "none",
                        "weights_bytes_per_step_all_ranks": bytes_all,
                        "l2": "no flush: every pass streams the stack's weights (GBs) > 126 MB L2",
-                       "cuda_graph": used_graph, "pdl": sq.get_option(sq.SQ_OPT_PDL),
-                       "weights_static": sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC)},
+                       "cuda_graph": used_graph, **launch_opts},
             "gpu_launches": launches_per_step * a.steps,
             "clocks": clocks,
             "roofline": roofline,
