@@ -45,16 +45,22 @@ def _newer(src: str, dst: str, deps) -> bool:
     return any(os.path.getmtime(p) > t for p in [src, *deps])
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), name: str = "") -> str:
+    """Compile every csrc/*.cu and link libsq.so.  `defines`/`name` build a tuning variant
+    into _lib/variants/libsq_<name>.so (development only)."""
+    obj_dir = OBJ_DIR if not name else os.path.join(OUT_DIR, "obj_" + name)
+    lib = LIB if not name else os.path.join(OUT_DIR, "variants", f"libsq_{name}.so")
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "libsq.h")]
     objs = []
     for src in sources:
-        obj = os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _newer(src, obj, headers):
-            cmd = [nvcc(), *CFLAGS, "-c", src, "-o", obj]
+            cmd = [nvcc(), *CFLAGS, *dflags, "-c", src, "-o", obj]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             if verbose:
@@ -65,15 +71,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
                 raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
             if verbose or ptxas_v:
                 sys.stderr.write(r.stderr)
-    if force or any(_newer(o, LIB, []) for o in objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    if force or any(_newer(o, lib, []) for o in objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link of libsq.so failed")
-    return LIB
+    return lib
 
 
 def main() -> None:
@@ -81,8 +87,10 @@ def main() -> None:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true")
+    ap.add_argument("--define", action="append", default=[])
+    ap.add_argument("--name", default="")
     a = ap.parse_args()
-    print(build(a.force, a.verbose, a.ptxas_v))
+    print(build(a.force or bool(a.name), a.verbose, a.ptxas_v, a.define, a.name))
 
 
 if __name__ == "__main__":

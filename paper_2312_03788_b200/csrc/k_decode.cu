@@ -32,16 +32,50 @@ namespace sq {
 namespace {
 
 constexpr int kGroup = 128;
-constexpr int BN = 64;          // rows per row block
+#ifndef SQ_DEC_BN
+#define SQ_DEC_BN 64
+#endif
+#ifndef SQ_DEC_CTAS
+#define SQ_DEC_CTAS 2
+#endif
+#ifndef SQ_DEC_NS1
+#define SQ_DEC_NS1 4
+#endif
+#ifndef SQ_DEC_NS2
+#define SQ_DEC_NS2 3
+#endif
+#ifndef SQ_DEC_ROWMAJOR
+#define SQ_DEC_ROWMAJOR 0  // 1: codes box traversed row by row (256 contiguous bytes per row)
+#endif
+#ifndef SQ_DEC_NOCOMPUTE
+#define SQ_DEC_NOCOMPUTE 0  // experiment: stream the operands but skip the math (bandwidth ceiling)
+#endif
+#ifndef SQ_DEC_ABLATE
+#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant (wrong results)
+#endif
+#ifndef SQ_DEC_CHAINS
+#define SQ_DEC_CHAINS 1  // independent MMA accumulator chains per row tile (1, 2 or 4)
+#endif
+#ifndef SQ_DEC_IL
+#define SQ_DEC_IL 0  // 1: load all 4 row tiles' codes first, then interleave their MMA chains
+#endif
+#ifndef SQ_DEC_SX
+#define SQ_DEC_SX 0  // 1: magic-offset MMAs + activation-sum correction (no per-code hsub/hfma)
+#endif
+#ifndef SQ_DEC_PF
+#define SQ_DEC_PF 0   // L2 prefetch distance in units ahead of the SMEM ring (0 = off)
+#endif
+constexpr int BN = SQ_DEC_BN;   // rows per row block (multiple of 16)
+constexpr int kRT = BN / 16;    // 16-row tiles per consumer warp
 constexpr int GPS = 4;          // groups per stage (= consumer warps)
 constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kMaxCtasPerSm = 2;
+constexpr int kMaxCtasPerSm = SQ_DEC_CTAS;
 
 template <int MT>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
-  static constexpr int NS = MT == 1 ? 4 : 3;
+  static constexpr int NS = MT == 1 ? SQ_DEC_NS1 : SQ_DEC_NS2;
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB
   static constexpr int XB = GPS * MPAD * kGroup * 2;      // 8 / 16 KB
   static constexpr int SZ = GPS * BN * 2;                 // 512 B
@@ -94,6 +128,14 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint3
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n"
+               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n"
+               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1) : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -102,26 +144,28 @@ __device__ __forceinline__ void consumer_sync() {
 }
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  // not volatile: ptxas/NVVM may schedule it early; the "memory" clobber keeps it after
+  // the mbarrier wait that makes the TMA data visible
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
   return v;
 }
 __device__ __forceinline__ uint16_t lds16(uint32_t addr) {
   uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr));
+  asm("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr) : "memory");
   return v;
 }
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                           uint32_t a3, uint32_t b0, uint32_t b1, bool bf16) {
   if (bf16) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
   } else {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -133,13 +177,13 @@ __device__ __forceinline__ void mma_16816_zc(float (&d)[4], uint32_t a0, uint32_
                                              uint32_t a3, uint32_t b0, uint32_t b1, bool bf16) {
   const float z = 0.0f;
   if (bf16) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%10,%10,%10,%10};\n"
         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(z));
   } else {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%10,%10,%10,%10};\n"
         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
@@ -247,13 +291,30 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
       // declared them static: stream the first stages before waiting on it.
       int pre = 0;
+      // L2 prefetch cursor, SQ_DEC_PF units ahead of the SMEM ring: more bytes in flight
+      // from HBM than the shared-memory ring alone can hold
+      int pf_u = u0, pf_rb = u0 / wk.upb, pf_g0 = (u0 % wk.upb) * GPS;
+      auto prefetch_next = [&]() {
+        if (SQ_DEC_PF > 0 && pf_u < u1) {
+          if (SQ_DEC_ROWMAJOR) tma_prefetch_3d(&tm_w, 0, pf_g0, pf_rb * BN);
+          else tma_prefetch_3d(&tm_w, 0, pf_rb * BN, pf_g0);
+          tma_prefetch_2d(&tm_s, pf_rb * BN, pf_g0);
+          tma_prefetch_2d(&tm_z, pf_rb * BN, pf_g0);
+          ++pf_u;
+          pf_g0 += GPS;
+          if (pf_g0 >= wk.upb * GPS) { pf_g0 = 0; ++pf_rb; }
+        }
+      };
+      if (SQ_DEC_PF > 0 && early_weights)
+        for (int q = 0; q < C::NS + SQ_DEC_PF; ++q) prefetch_next();
       if (early_weights) {
         int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
         for (; pre < C::NS && u0 + pre < u1; ++pre) {
           const uint32_t st = sbase + pre * C::STAGE;
           const uint32_t fb = bar_full + 8 * pre;
           mbar_expect_tx(fb, C::STAGE);
-          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+          if (SQ_DEC_ROWMAJOR) tma_3d(st, &tm_w, fb, 0, g0, rb * BN);
+          else tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
           tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
           tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
           g0 += GPS;
@@ -261,6 +322,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
+      if (SQ_DEC_PF > 0 && !early_weights)
+        for (int q = 0; q < C::NS + SQ_DEC_PF; ++q) prefetch_next();
       int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
       int s = 0;
       uint32_t ph = 0;
@@ -272,10 +335,12 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         } else {
           mbar_wait(bar_empty + 8 * s, ph ^ 1);
           mbar_expect_tx(fb, C::STAGE);
-          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+          if (SQ_DEC_ROWMAJOR) tma_3d(st, &tm_w, fb, 0, g0, rb * BN);
+          else tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
           tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
           tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
           tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+          prefetch_next();
         }
         if (++s == C::NS) { s = 0; ph ^= 1; }
         g0 += GPS;
@@ -287,9 +352,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   // ===================== consumers: warp w = group w of each stage =====================
   const int r = lane / 4, j = lane % 4;
-  float acc[4][MT][4];
+  float acc[kRT][MT][4];
 #pragma unroll
-  for (int rt = 0; rt < 4; ++rt)
+  for (int rt = 0; rt < kRT; ++rt)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -305,6 +370,16 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
   for (int u = u0; u < u1; ++u) {
     mbar_wait(bar_full + 8 * s, ph);
     const uint32_t st = sbase + s * C::STAGE;
+#if SQ_DEC_NOCOMPUTE
+    if (true) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+      if (++s == C::NS) { s = 0; ph ^= 1; }
+      ++pos;
+      if (pos == wk.upb) { ++rb; pos = 0; seg_begin_pos = 0; first_seg = false; }
+      continue;
+    }
+#endif
 
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
@@ -326,36 +401,195 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         xb[mt][w][3] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x7632u);  // (x3, x7)
       }
     }
-    const uint32_t cbase = st + warp * (BN * 64) + r * 64 + j * 16;
+#if SQ_DEC_SX
+    // activation sums of this group for this lane's tokens: even-k and odd-k positions
+    float sxe[MT][2], sxo[MT][2];
+    {
+      const uint32_t kOnes = kBF16 ? 0x3F803F80u : 0x3C003C00u;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        float se[4], so[4];
+        mma_16816_zc(se, kOnes, kOnes, kOnes, kOnes, xb[mt][0][0], xb[mt][0][2], kBF16);
+        mma_16816_zc(so, kOnes, kOnes, kOnes, kOnes, xb[mt][0][1], xb[mt][0][3], kBF16);
+#pragma unroll
+        for (int w = 1; w < 4; ++w) {
+          mma_16816(se, kOnes, kOnes, kOnes, kOnes, xb[mt][w][0], xb[mt][w][2], kBF16);
+          mma_16816(so, kOnes, kOnes, kOnes, kOnes, xb[mt][w][1], xb[mt][w][3], kBF16);
+        }
+        sxe[mt][0] = se[0]; sxe[mt][1] = se[1];
+        sxo[mt][0] = so[0]; sxo[mt][1] = so[1];
+      }
+    }
+#endif
+    // codes of this warp's group: [group][row][64 B] (default) or [row][group][64 B]
+    const uint32_t cbase = SQ_DEC_ROWMAJOR ? st + warp * 64 + r * (GPS * 64) + j * 16
+                                           : st + warp * (BN * 64) + r * 64 + j * 16;
+    constexpr int kRowStride = SQ_DEC_ROWMAJOR ? GPS * 64 : 64;
     const uint32_t sbs = st + C::CODES + C::XB + warp * (BN * 2) + r * 2;
     const uint32_t sbz = sbs + C::SZ;
+#if SQ_DEC_IL
+    {
+      uint32_t wa[kRT][4], wb[kRT][4], zsA[kRT], zfA[kRT], zsB[kRT], zfB[kRT];
+      float dA[kRT], dB[kRT];
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt) {
-      const uint4 ca = lds128(cbase + rt * 16 * 64);
-      const uint4 cb = lds128(cbase + (rt * 16 + 8) * 64);
+      for (int rt = 0; rt < kRT; ++rt) {
+        const uint4 ca = lds128(cbase + rt * 16 * kRowStride);
+        const uint4 cb = lds128(cbase + (rt * 16 + 8) * kRowStride);
+        wa[rt][0] = ca.x; wa[rt][1] = ca.y; wa[rt][2] = ca.z; wa[rt][3] = ca.w;
+        wb[rt][0] = cb.x; wb[rt][1] = cb.y; wb[rt][2] = cb.z; wb[rt][3] = cb.w;
+        dA[rt] = __half2float(__ushort_as_half(lds16(sbs + rt * 32)));
+        dB[rt] = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
+        zero_consts<kBF16>(lds16(sbz + rt * 32), zsA[rt], zfA[rt]);
+        zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB[rt], zfB[rt]);
+      }
+      float g[kRT][MT][4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+#pragma unroll
+        for (int rt = 0; rt < kRT; ++rt) {
+          uint32_t hA[4], hB[4];
+          dequant_word<kBF16>(wa[rt][w], zsA[rt], zfA[rt], hA);
+          dequant_word<kBF16>(wb[rt][w], zsB[rt], zfB[rt], hB);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            if (w == 0) {
+              mma_16816_zc(g[rt][mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+            } else {
+              mma_16816(g[rt][mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+            }
+            mma_16816(g[rt][mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
+          }
+        }
+      }
+#pragma unroll
+      for (int rt = 0; rt < kRT; ++rt)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          acc[rt][mt][0] = fmaf(g[rt][mt][0], dA[rt], acc[rt][mt][0]);
+          acc[rt][mt][1] = fmaf(g[rt][mt][1], dA[rt], acc[rt][mt][1]);
+          acc[rt][mt][2] = fmaf(g[rt][mt][2], dB[rt], acc[rt][mt][2]);
+          acc[rt][mt][3] = fmaf(g[rt][mt][3], dB[rt], acc[rt][mt][3]);
+        }
+    }
+    if (false)
+#endif
+#pragma unroll
+    for (int rt = 0; rt < kRT; ++rt) {
+      const uint4 ca = lds128(cbase + rt * 16 * kRowStride);
+      const uint4 cb = lds128(cbase + (rt * 16 + 8) * kRowStride);
       const float dA = __half2float(__ushort_as_half(lds16(sbs + rt * 32)));
       const float dB = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
+#if SQ_DEC_SX
+      {
+        const float zA = __half2float(__ushort_as_half(lds16(sbz + rt * 32)));
+        const float zB = __half2float(__ushort_as_half(lds16(sbz + rt * 32 + 16)));
+        const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
+        const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+        float ge[MT][4], go[MT][4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint32_t la0, la1, ha0, ha1, lb0, lb1, hb0, hb1;
+          if (!kBF16) {
+            const uint32_t ta = wa[w] >> 8, tb = wb[w] >> 8;
+            la0 = lop3_and_or(wa[w], 0x000F000Fu, 0x64006400u);  // 1024 + (e0, e4)
+            la1 = lop3_and_or(ta, 0x000F000Fu, 0x64006400u);     // 1024 + (e2, e6)
+            ha0 = lop3_and_or(wa[w], 0x00F000F0u, 0x64006400u);  // 1024 + 16 (e1, e5)
+            ha1 = lop3_and_or(ta, 0x00F000F0u, 0x64006400u);     // 1024 + 16 (e3, e7)
+            lb0 = lop3_and_or(wb[w], 0x000F000Fu, 0x64006400u);
+            lb1 = lop3_and_or(tb, 0x000F000Fu, 0x64006400u);
+            hb0 = lop3_and_or(wb[w], 0x00F000F0u, 0x64006400u);
+            hb1 = lop3_and_or(tb, 0x00F000F0u, 0x64006400u);
+          } else {
+            la0 = lop3_and_or(wa[w], 0x000F000Fu, 0x43004300u);
+            la1 = lop3_and_or(wa[w] >> 8, 0x000F000Fu, 0x43004300u);
+            ha0 = lop3_and_or(wa[w] >> 4, 0x000F000Fu, 0x43004300u);
+            ha1 = lop3_and_or(wa[w] >> 12, 0x000F000Fu, 0x43004300u);
+            lb0 = lop3_and_or(wb[w], 0x000F000Fu, 0x43004300u);
+            lb1 = lop3_and_or(wb[w] >> 8, 0x000F000Fu, 0x43004300u);
+            hb0 = lop3_and_or(wb[w] >> 4, 0x000F000Fu, 0x43004300u);
+            hb1 = lop3_and_or(wb[w] >> 12, 0x000F000Fu, 0x43004300u);
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            if (w == 0) {
+              mma_16816_zc(ge[mt], la0, lb0, la1, lb1, xb[mt][w][0], xb[mt][w][2], kBF16);
+              mma_16816_zc(go[mt], ha0, hb0, ha1, hb1, xb[mt][w][1], xb[mt][w][3], kBF16);
+            } else {
+              mma_16816(ge[mt], la0, lb0, la1, lb1, xb[mt][w][0], xb[mt][w][2], kBF16);
+              mma_16816(go[mt], ha0, hb0, ha1, hb1, xb[mt][w][1], xb[mt][w][3], kBF16);
+            }
+          }
+        }
+        // sum_k X (q - Z) = ge + go/16 - (1024+Z) SXe - (64+Z) SXo   (fp16 magic)
+        //                 = ge + go    - (128+Z) (SXe + SXo)          (bf16 magic)
+        const float osc = kBF16 ? 1.0f : 0.0625f;
+        const float ceA = -((kBF16 ? 128.0f : 1024.0f) + zA), coA = -((kBF16 ? 128.0f : 64.0f) + zA);
+        const float ceB = -((kBF16 ? 128.0f : 1024.0f) + zB), coB = -((kBF16 ? 128.0f : 64.0f) + zB);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float ce = i < 2 ? ceA : ceB, co = i < 2 ? coA : coB, d = i < 2 ? dA : dB;
+            float v = fmaf(go[mt][i], osc, ge[mt][i]);
+            v = fmaf(ce, sxe[mt][i & 1], v);
+            v = fmaf(co, sxo[mt][i & 1], v);
+            acc[rt][mt][i] = fmaf(v, d, acc[rt][mt][i]);
+          }
+        }
+        continue;
+      }
+#endif
       uint32_t zsA, zfA, zsB, zfB;
       zero_consts<kBF16>(lds16(sbz + rt * 32), zsA, zfA);
       zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB, zfB);
       const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
       const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
-      float g[MT][4];
+      constexpr int NC = SQ_DEC_CHAINS;
+      float gc[MT][NC][4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t hA[4], hB[4];
+#if SQ_DEC_ABLATE == 2
+        hA[0] = wa[w]; hA[1] = wa[w] >> 8; hA[2] = wa[w] >> 4; hA[3] = wa[w] >> 12;
+        hB[0] = wb[w]; hB[1] = wb[w] >> 8; hB[2] = wb[w] >> 4; hB[3] = wb[w] >> 12;
+#else
         dequant_word<kBF16>(wa[w], zsA, zfA, hA);
         dequant_word<kBF16>(wb[w], zsB, zfB, hB);
+#endif
+#if SQ_DEC_ABLATE == 1
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            gc[mt][0][i] = (w == 0 ? 0.0f : gc[mt][0][i]) +
+                           __uint_as_float((hA[i] ^ hB[i] ^ xb[mt][w][i]) & 0x3FFFFFFFu);
+        if (false)
+#endif
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          if (w == 0) {
-            mma_16816_zc(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
-          } else {
-            mma_16816(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = 2 * w + h, ch = q % NC;  // q-th MMA of the group -> chain ch
+            if (q < NC) {
+              mma_16816_zc(gc[mt][ch], hA[2 * h], hB[2 * h], hA[2 * h + 1], hB[2 * h + 1],
+                           xb[mt][w][2 * h], xb[mt][w][2 * h + 1], kBF16);
+            } else {
+              mma_16816(gc[mt][ch], hA[2 * h], hB[2 * h], hA[2 * h + 1], hB[2 * h + 1],
+                        xb[mt][w][2 * h], xb[mt][w][2 * h + 1], kBF16);
+            }
           }
-          mma_16816(g[mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
         }
       }
+      float g[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float v = gc[mt][0][i];
+#pragma unroll
+          for (int ch = 1; ch < NC; ++ch) v += gc[mt][ch][i];
+          g[mt][i] = v;
+        }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         acc[rt][mt][0] = fmaf(g[mt][0], dA, acc[rt][mt][0]);
@@ -381,7 +615,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     if (warp > 0) {
       float* rw = red + (warp - 1) * C::MPAD * BN;
 #pragma unroll
-      for (int rt = 0; rt < 4; ++rt)
+      for (int rt = 0; rt < kRT; ++rt)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
@@ -394,7 +628,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     consumer_sync();
     if (warp == 0) {
 #pragma unroll
-      for (int rt = 0; rt < 4; ++rt)
+      for (int rt = 0; rt < kRT; ++rt)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
@@ -415,7 +649,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
     consumer_sync();
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt)
+    for (int rt = 0; rt < kRT; ++rt)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -525,9 +759,9 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
   {
-    const uint64_t d[3] = {64, (uint64_t)N, (uint64_t)G};
-    const uint64_t s[2] = {(uint64_t)K / 2, 64};
-    const uint32_t b[3] = {64, BN, GPS};
+    const uint64_t d[3] = {64, SQ_DEC_ROWMAJOR ? (uint64_t)G : (uint64_t)N, SQ_DEC_ROWMAJOR ? (uint64_t)N : (uint64_t)G};
+    const uint64_t s[2] = {SQ_DEC_ROWMAJOR ? 64 : (uint64_t)K / 2, SQ_DEC_ROWMAJOR ? (uint64_t)K / 2 : 64};
+    const uint32_t b[3] = {64, SQ_DEC_ROWMAJOR ? (uint32_t)GPS : (uint32_t)BN, SQ_DEC_ROWMAJOR ? (uint32_t)BN : (uint32_t)GPS};
     if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, Wq, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
       *why = "tensor map (codes)";
       return cudaErrorInvalidValue;

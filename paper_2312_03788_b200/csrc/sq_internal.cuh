@@ -37,13 +37,13 @@ int option(int opt);
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t and_mask, uint32_t or_mask) {
   uint32_t r;
   // r = (a & b) | c   -> immLut = (0xF0 & 0xCC) | 0xAA = 0xEA
-  asm volatile("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(a), "r"(and_mask), "r"(or_mask));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(a), "r"(and_mask), "r"(or_mask));
   return r;
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
-  asm volatile("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
 

@@ -21,7 +21,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsq.so")
+# SQ_LIB overrides the in-tree library (development A/B of tuning variants only)
+LIB_PATH = os.environ.get("SQ_LIB") or os.path.join(_HERE, "_lib", "libsq.so")
 
 SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
 SQ_F16, SQ_BF16 = 0, 1
