@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="collective backend (gloo: test the TP path "
+                    "with several ranks on one GPU, together with --one-device --no-graph)")
+    ap.add_argument("--one-device", action="store_true", help="all ranks on cuda:0 (testing only)")
     return ap.parse_args()
 
 
@@ -215,11 +218,16 @@ def main():
 
     from paper_2312_03788_b200 import sq, stack, tp
 
+    if a.one_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(a.backend)
         pg = dist.group.WORLD
     peaks, peaks_src = load_peaks()
     ms = [int(x) for x in a.decode_m.split(",")]
@@ -316,20 +324,29 @@ def main():
                 "kernel": "sq::decode_kernel (TMA-fed mma.sync W4A16, persistent stream-K)",
                 "peak_source": f"{peaks_src} hbm_gbs", "bytes_per_launch": dec_bytes_launch}
 
-    # per-M breakdown (graph per M), for the report
+    # per-M breakdown (one graph per M unless --no-graph), for the report
     per_m = {}
     for b in bufs:
-        g2 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g2):
-            stack.run_pass(st, b)
+        g2 = None
+        if not a.no_graph:
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2):
+                stack.run_pass(st, b)
+
+        def one(b=b, g2=g2):
+            if g2 is not None:
+                g2.replay()
+            else:
+                stack.run_pass(st, b)
+
         for _ in range(2):
-            g2.replay()
-        torch.cuda.synchronize()
+            one()
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = max(3, a.steps // 3)
         e0.record()
         for _ in range(reps):
-            g2.replay()
+            one()
         e1.record()
         torch.cuda.synchronize()
         tm = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / reps)
