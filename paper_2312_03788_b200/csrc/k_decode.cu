@@ -47,6 +47,9 @@ constexpr int kGroup = 128;
 #ifndef SQ_DEC_ROWMAJOR
 #define SQ_DEC_ROWMAJOR 0  // 1: codes box traversed row by row (256 contiguous bytes per row)
 #endif
+#ifndef SQ_DEC_NOLOAD
+#define SQ_DEC_NOLOAD 0  // experiment: after the first NS stages, recompute on resident data (compute ceiling)
+#endif
 #ifndef SQ_DEC_NOCOMPUTE
 #define SQ_DEC_NOCOMPUTE 0  // experiment: stream the operands but skip the math (bandwidth ceiling)
 #endif
@@ -67,7 +70,11 @@ constexpr int kGroup = 128;
 #endif
 constexpr int BN = SQ_DEC_BN;   // rows per row block (multiple of 16)
 constexpr int kRT = BN / 16;    // 16-row tiles per consumer warp
-constexpr int GPS = 4;          // groups per stage (= consumer warps)
+#ifndef SQ_DEC_GPW
+#define SQ_DEC_GPW 1  // groups per consumer warp per stage
+#endif
+constexpr int GPW = SQ_DEC_GPW;
+constexpr int GPS = 4 * GPW;    // groups per stage (4 consumer warps x GPW)
 constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kMaxCtasPerSm = SQ_DEC_CTAS;
@@ -332,6 +339,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const uint32_t fb = bar_full + 8 * s;
         if (i < pre) {
           tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
+        } else if (SQ_DEC_NOLOAD && i >= C::NS) {
+          mbar_wait(bar_empty + 8 * s, ph ^ 1);
+          mbar_arrive(fb);
         } else {
           mbar_wait(bar_empty + 8 * s, ph ^ 1);
           mbar_expect_tx(fb, C::STAGE);
@@ -381,11 +391,14 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
 #endif
 
+#pragma unroll
+    for (int gi = 0; gi < GPW; ++gi) {
+    const int grp = warp + kConsumerWarps * gi;  // group of the stage this pass works on
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
-      const int R = (warp * C::MPAD + r + 8 * mt) * 2 + (j >> 1);  // 128-byte row of the swizzled box
+      const int R = (grp * C::MPAD + r + 8 * mt) * 2 + (j >> 1);  // 128-byte row of the swizzled box
       const uint32_t rowaddr = st + C::CODES + R * 128;
       uint32_t xv[16];
 #pragma unroll
@@ -422,10 +435,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
 #endif
     // codes of this warp's group: [group][row][64 B] (default) or [row][group][64 B]
-    const uint32_t cbase = SQ_DEC_ROWMAJOR ? st + warp * 64 + r * (GPS * 64) + j * 16
-                                           : st + warp * (BN * 64) + r * 64 + j * 16;
+    const uint32_t cbase = SQ_DEC_ROWMAJOR ? st + grp * 64 + r * (GPS * 64) + j * 16
+                                           : st + grp * (BN * 64) + r * 64 + j * 16;
     constexpr int kRowStride = SQ_DEC_ROWMAJOR ? GPS * 64 : 64;
-    const uint32_t sbs = st + C::CODES + C::XB + warp * (BN * 2) + r * 2;
+    const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
     const uint32_t sbz = sbs + C::SZ;
 #if SQ_DEC_IL
     {
@@ -597,6 +610,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         acc[rt][mt][2] = fmaf(g[mt][2], dB, acc[rt][mt][2]);
         acc[rt][mt][3] = fmaf(g[mt][3], dB, acc[rt][mt][3]);
       }
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(bar_empty + 8 * s);

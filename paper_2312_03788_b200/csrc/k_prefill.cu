@@ -31,15 +31,26 @@ namespace sq {
 
 namespace {
 
+#ifndef SQ_PRE_2CTA
+#define SQ_PRE_2CTA 0  // 1: CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles)
+#endif
 constexpr int BM = 128;        // weight rows per tile (MMA M, TMEM lanes)
 constexpr int BT = 256;        // tokens per tile (MMA N max)
 constexpr int BK = 64;         // k per X stage / A stage
 constexpr int kGroup = 128;
 constexpr int NSX = 4;         // X stages (SMEM)
-constexpr int NSC = 4;         // code+scale stages (SMEM), one group each
-constexpr int NSA = 4;         // dequantized-A stages (TMEM)
-constexpr int kThreads = 256;  // 8 warps
+constexpr int NSC = 8;         // code+scale stages (SMEM), one group each
+#ifndef SQ_PRE_NSA
+#define SQ_PRE_NSA 4
+#endif
+constexpr int NSA = SQ_PRE_NSA;  // dequantized-A stages (TMEM, 32 columns each; D + A <= 512)
+#ifndef SQ_PRE_DQW
+#define SQ_PRE_DQW 8  // dequant/epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter)
+#endif
+constexpr int kDQW = SQ_PRE_DQW;
 constexpr int kDequantWarp0 = 4;
+constexpr int kThreads = (kDequantWarp0 + kDQW) * 32;
+constexpr int kColSplit = kDQW / 4;  // warps sharing a lane quarter split the k / token columns
 
 constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
 constexpr int C_STAGE_BYTES = BM * (kGroup / 2);  // 8 KB
@@ -73,6 +84,34 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+#ifndef SQ_PRE_ABLATE
+#define SQ_PRE_ABLATE 0  // development: 1 = no X loads, 2 = no code loads, 4 = no dequant (timing only)
+#endif
+#ifndef SQ_PRE_TRACE
+#define SQ_PRE_TRACE 0  // development: per-CTA cycles spent in each barrier wait
+#endif
+#if SQ_PRE_TRACE
+__device__ unsigned long long g_pre_trace[1024 * 8];
+#define PTW(slot, call)                   \
+  do {                                    \
+    const long long t_ = clock64();       \
+    call;                                 \
+    tr[slot] += clock64() - t_;           \
+  } while (0)
+#else
+#define PTW(slot, call) call
+#endif
+#if SQ_PRE_TRACE
+__device__ long long g_pre_ts[16 * 1024];
+#define PTS(row, idx)                                                              \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (idx) < 1024) g_pre_ts[(row) * 1024 + (idx)] = clock64(); \
+  } while (0)
+#else
+#define PTS(row, idx) \
+  do {                \
+  } while (0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -94,6 +133,10 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -127,6 +170,14 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),
       "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),
       "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() {
@@ -204,7 +255,7 @@ template <bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
-               uint16_t* __restrict__ Y, int M, int N, int K) {
+               uint16_t* __restrict__ Y, int M, int N, int K, int early_weights) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -229,10 +280,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
-    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), 4); }
-    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), 4); mbar_init(a_empty(i), 1); }
+    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), kDQW); }
+    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), kDQW); mbar_init(a_empty(i), 1); }
     mbar_init(d_full, 1);
-    mbar_init(d_empty, 4);
+    mbar_init(d_empty, kDQW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
@@ -252,29 +303,49 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_launch_dependents();
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer: activations =====================
     if (lane == 0) {
-      int xs = 0, cs = 0;
-      uint32_t xph = 0, cph = 0;
+      pdl_wait();  // X may be the previous kernel's output
+      int xs = 0;
+      uint32_t xph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int n0 = (tile / m_tiles) * BM;
         const int m0 = (tile % m_tiles) * BT;
         for (int kb = 0; kb < num_kb; ++kb) {
-          if ((kb & 1) == 0) {
-            const int g = kb >> 1;
-            mbar_wait(c_empty(cs), cph ^ 1);
+          mbar_wait(x_empty(xs), xph ^ 1);
+          PTS(5, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
+          if (SQ_PRE_ABLATE & 1) {
+            mbar_arrive(x_full(xs));
+          } else {
+            mbar_expect_tx(x_full(xs), X_STAGE_BYTES);
+            tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
+          }
+          if (++xs == NSX) { xs = 0; xph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===================== TMA producer: packed codes + Δ/Z rows (own ring, runs ahead) ====
+    if (lane == 0) {
+      if (!early_weights) pdl_wait();
+      int cs = 0;
+      uint32_t cph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int n0 = (tile / m_tiles) * BM;
+        for (int g = 0; g < G; ++g) {
+          mbar_wait(c_empty(cs), cph ^ 1);
+          PTS(4, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
+          if (SQ_PRE_ABLATE & 2) {
+            mbar_arrive(c_full(cs));
+          } else {
             mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
             tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
             tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
             tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
-            if (++cs == NSC) { cs = 0; cph ^= 1; }
           }
-          mbar_wait(x_empty(xs), xph ^ 1);
-          mbar_expect_tx(x_full(xs), X_STAGE_BYTES);
-          tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
-          if (++xs == NSX) { xs = 0; xph ^= 1; }
+          if (++cs == NSC) { cs = 0; cph ^= 1; }
         }
       }
     }
@@ -283,16 +354,22 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     if (lane == 0) {
       int xs = 0, as = 0;
       uint32_t xph = 0, aph = 0, dph = 0;
+#if SQ_PRE_TRACE
+      unsigned long long tr[4] = {0, 0, 0, 0};
+      const long long t_all = clock64();
+#endif
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int m0 = (tile % m_tiles) * BT;
         const int n_mma = min(BT, ((M - m0) + 15) & ~15);
         const uint32_t idesc = make_idesc(kBF16, n_mma);
-        mbar_wait(d_empty, dph ^ 1);  // epilogue has drained the accumulator
+        PTW(0, mbar_wait(d_empty, dph ^ 1));  // epilogue has drained the accumulator
         dph ^= 1;
         tc_fence_after();
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(a_full(as), aph);
-          mbar_wait(x_full(xs), xph);
+          PTW(1, mbar_wait(a_full(as), aph));
+          PTS(0, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
+          PTW(2, mbar_wait(x_full(xs), xph));
+          PTS(1, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
           tc_fence_after();
           const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE_BYTES;
 #pragma unroll
@@ -308,25 +385,42 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         }
         tc_commit(d_full);
       }
+#if SQ_PRE_TRACE
+      tr[3] = clock64() - t_all;
+      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + i] = tr[i];
+#endif
     }
   } else if (warp >= kDequantWarp0) {
     // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
-    const int q = warp - kDequantWarp0;  // TMEM sub-partition (warp % 4)
+    const int q = (warp - kDequantWarp0) % 4;   // TMEM sub-partition (warp % 4)
+    const int ch = (warp - kDequantWarp0) / 4;  // column split among warps of one quarter
     const int row = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int cs = 0, as = 0;
     uint32_t cph = 0, aph = 0, dph = 0;
+#if SQ_PRE_TRACE
+    unsigned long long tr[4] = {0, 0, 0, 0};
+    const long long t_all = clock64();
+#endif
+    uint32_t abl_sink = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int n0 = (tile / m_tiles) * BM;
       const int m0 = (tile % m_tiles) * BT;
       for (int g = 0; g < G; ++g) {
-        mbar_wait(c_full(cs), cph);
+        PTW(0, mbar_wait(c_full(cs), cph));
+        if (lane == 0 && warp == kDequantWarp0) PTS(2, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
         const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
         // SWIZZLE_64B: 16-byte chunk c of this row sits at chunk c ^ ((row >> 1) & 3)
         const int sw = (row >> 1) & 3;
-        uint4 cv[4];
+        // this warp's 16-byte chunks of the group row: k-block h uses chunks 2h .. 2h+1,
+        // split across the kColSplit warps of this lane quarter
+        constexpr int kCh = 4 / kColSplit;
+        uint4 cv[kCh];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cv[c] = *reinterpret_cast<const uint4*>(crow + ((c ^ sw) << 4));
+        for (int c = 0; c < kCh; ++c) {
+          const int cc = (c / (2 / kColSplit)) * 2 + (kColSplit == 2 ? ch : (c % 2));
+          cv[c] = *reinterpret_cast<const uint4*>(crow + ((cc ^ sw) << 4));
+        }
         const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
         const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
         __syncwarp();
@@ -341,28 +435,61 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const float df = __half2float(__ushort_as_half(sbits));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // two 64-k stages per group
-          const uint32_t words[8] = {cv[2 * h].x,     cv[2 * h].y,     cv[2 * h].z,     cv[2 * h].w,
-                                     cv[2 * h + 1].x, cv[2 * h + 1].y, cv[2 * h + 1].z, cv[2 * h + 1].w};
-          uint32_t a[32];
+          constexpr int kW = 8 / kColSplit;  // 32-bit code words of this warp per k-block
+          uint32_t words[kW];
 #pragma unroll
-          for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
-          mbar_wait(a_empty(as), aph ^ 1);
+          for (int c = 0; c < kW / 4; ++c) {
+            const uint4 v = cv[h * (kW / 4) + c];
+            words[4 * c] = v.x; words[4 * c + 1] = v.y; words[4 * c + 2] = v.z; words[4 * c + 3] = v.w;
+          }
+          uint32_t a[4 * kW];
+          if (SQ_PRE_ABLATE & 16) {
+#pragma unroll
+            for (int i = 0; i < 4 * kW; ++i) a[i] = words[i % kW] + i;
+          } else {
+#pragma unroll
+            for (int wd = 0; wd < kW; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+          }
+          PTW(1, mbar_wait(a_empty(as), aph ^ 1));
+          if (lane == 0 && warp == kDequantWarp0)
+            PTS(3, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + 2 * g + h);
+          if (SQ_PRE_ABLATE & 8) {
+#pragma unroll
+            for (int i = 0; i < 4 * kW; ++i) abl_sink ^= a[i];
+          }
+          if (SQ_PRE_ABLATE & 12) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full(as));
+            if (++as == NSA) { as = 0; aph ^= 1; }
+            continue;
+          }
           tc_fence_after();
-          tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2), a);
+          if constexpr (kColSplit == 1)
+            tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2),
+                               *reinterpret_cast<const uint32_t(*)[32]>(a));
+          else
+            tmem_st_32x32b_x16(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2) + ch * 16, a);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(a_full(as));
+          if (lane == 0)
+            PTS(6 + warp - kDequantWarp0, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + 2 * g + h);
           if (++as == NSA) { as = 0; aph ^= 1; }
         }
       }
       // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
-      mbar_wait(d_full, dph);
+      pdl_wait();  // (returns at once after the first tile) Y may be read by the previous kernel
+      PTW(2, mbar_wait(d_full, dph));
       dph ^= 1;
+#if SQ_PRE_TRACE
+      const long long t_ep = clock64();
+#endif
       tc_fence_after();
       const int n = n0 + row;
       const int mt = min(BT, M - m0);
-      for (int c0 = 0; c0 < mt; c0 += 16) {
+      // warps sharing a lane quarter take alternating 16-token column blocks
+      for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
         uint32_t v[16];
         tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
         tmem_ld_wait();
@@ -382,7 +509,17 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(d_empty);
+#if SQ_PRE_TRACE
+      tr[3] += clock64() - t_ep;
+#endif
     }
+    if ((SQ_PRE_ABLATE & 8) && abl_sink == 0x9E3779B9u) Y[0] = 1;
+#if SQ_PRE_TRACE
+    if (warp == kDequantWarp0 && lane == 0)
+      for (int i = 0; i < 3; ++i) g_pre_trace[blockIdx.x * 8 + 4 + i] = tr[i];
+    if (warp == kDequantWarp0 && lane == 0) g_pre_trace[blockIdx.x * 8 + 7] = tr[3];
+    (void)t_all;
+#endif
   }
 
   tc_fence_before();
@@ -390,6 +527,321 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ 2-CTA (CTA-pair) variant
+// Same dataflow, but a cluster of two CTAs on a TPC computes a 256-row x 256-token tile
+// with tcgen05.mma.cta_group::2 (M = 256): each CTA dequantizes its own 128 weight rows
+// into its own TMEM and loads half of the token tile into its own shared memory, so
+// every SM reads and writes half the activation bytes per MMA -- the 1-CTA kernel is
+// shared-memory-bandwidth bound on the X operand (TMA write + MMA read).
+namespace p2 {
+constexpr int BT2 = 256;                           // tokens per tile (MMA N)
+constexpr int NSX = 6;
+constexpr int NSC = 8;
+constexpr int NSA = SQ_PRE_NSA;
+constexpr int X_STAGE = (BT2 / 2) * BK * 2;        // 16 KB: this CTA's half of the tokens
+constexpr int OFF_X = 0;
+constexpr int OFF_C = OFF_X + NSX * X_STAGE;
+constexpr int OFF_S = OFF_C + NSC * C_STAGE_BYTES;
+constexpr int OFF_Z = OFF_S + NSC * SZ_BYTES;
+constexpr int OFF_BAR = OFF_Z + NSC * SZ_BYTES;
+constexpr int NUM_BARS = 2 * NSX + 2 * NSC + 2 * NSA + 2;
+constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+constexpr int SMEM = OFF_TMEM + 16;
+constexpr int SMEM_ALLOC = SMEM + 1024;
+}  // namespace p2
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// arrive on the barrier at the same offset in CTA 0 of the pair (bit 24 of a
+// shared::cluster address selects the peer CTA)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  // default (.release.cta) semantics: no GPU-scope membar; the TMEM data is ordered by
+  // tcgen05.wait::st + tcgen05.fence::before_thread_sync before this arrive
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar & 0xFEFFFFFFu) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n"
+      ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill2_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
+                uint16_t* __restrict__ Y, int M, int N, int K, int early_weights) {
+  constexpr int NSX = p2::NSX, NSC = p2::NSC, NSA = p2::NSA, BT2 = p2::BT2, X_STAGE = p2::X_STAGE;
+  constexpr int OFF_X = p2::OFF_X, OFF_C = p2::OFF_C, OFF_S = p2::OFF_S, OFF_Z = p2::OFF_Z;
+  constexpr int OFF_BAR = p2::OFF_BAR, OFF_TMEM = p2::OFF_TMEM;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto x_full = [&](int i) { return bar0 + 8u * i; };
+  auto x_empty = [&](int i) { return bar0 + 8u * (NSX + i); };
+  auto c_full = [&](int i) { return bar0 + 8u * (2 * NSX + i); };
+  auto c_empty = [&](int i) { return bar0 + 8u * (2 * NSX + NSC + i); };
+  auto a_full = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + i); };
+  auto a_empty = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + NSA + i); };
+  const uint32_t d_full = bar0 + 8u * (2 * NSX + 2 * NSC + 2 * NSA);
+  const uint32_t d_empty = d_full + 8u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / 2, num_clusters = gridDim.x / 2;
+  const int n_tiles = (N + 2 * BM - 1) / (2 * BM);
+  const int m_tiles = (M + BT2 - 1) / BT2;
+  const int num_tiles = n_tiles * m_tiles;
+  const int num_kb = K / BK;
+  const int G = K / kGroup;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
+    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), kDQW); }
+    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), 2 * kDQW); mbar_init(a_empty(i), 1); }
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 2 * kDQW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_x);
+    prefetch_tmap(&tm_w);
+    prefetch_tmap(&tm_s);
+    prefetch_tmap(&tm_z);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_launch_dependents();
+
+  auto tile_n_mma = [&](int m0) { return min(BT2, ((M - m0) + 31) & ~31); };
+
+  if (warp == 0) {
+    // ===================== TMA producer: this CTA's half of the token tile =====================
+    if (lane == 0) {
+      pdl_wait();
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int m0 = (tile % m_tiles) * BT2;
+        const int half = tile_n_mma(m0) / 2;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(x_empty(xs), xph ^ 1);
+          if (leader) mbar_expect_tx(x_full(xs), 2 * X_STAGE);
+          tma_load_2d_pair(sbase + OFF_X + xs * X_STAGE, &tm_x, x_full(xs), kb * BK,
+                           m0 + (int)rank * half);
+          if (++xs == NSX) { xs = 0; xph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===================== TMA producer: this CTA's 128 weight rows =====================
+    if (lane == 0) {
+      if (!early_weights) pdl_wait();
+      int cs = 0;
+      uint32_t cph = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int n0 = (tile / m_tiles) * 2 * BM + (int)rank * BM;
+        for (int g = 0; g < G; ++g) {
+          mbar_wait(c_empty(cs), cph ^ 1);
+          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
+          tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
+          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
+          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
+          if (++cs == NSC) { cs = 0; cph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer: one thread of the leader CTA =====================
+    if (leader && lane == 0) {
+      int xs = 0, as = 0;
+      uint32_t xph = 0, aph = 0, dph = 0;
+#if SQ_PRE_TRACE
+      unsigned long long tr[4] = {0, 0, 0, 0};
+      const long long t_all = clock64();
+#endif
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int m0 = (tile % m_tiles) * BT2;
+        const int n_mma = tile_n_mma(m0);
+        uint32_t idesc = make_idesc(kBF16, n_mma);
+        idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(2 * BM >> 4) << 24);  // M = 256
+        PTW(0, mbar_wait(d_empty, dph ^ 1));  // both epilogues have drained the accumulators
+        dph ^= 1;
+        tc_fence_after();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          PTW(1, mbar_wait(a_full(as), aph));
+          PTW(2, mbar_wait(x_full(xs), xph));
+          tc_fence_after();
+          const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t a_tmem = tmem_base + A_COL + (uint32_t)as * (BK / 2) + (uint32_t)kk * 8;
+            tc_mma_ts_pair(tmem_base + D_COL, a_tmem, make_sw128_desc(xaddr + kk * 32), idesc,
+                           (kb | kk) ? 1u : 0u);
+          }
+          tc_commit_pair(x_empty(xs));
+          tc_commit_pair(a_empty(as));
+          if (++xs == NSX) { xs = 0; xph ^= 1; }
+          if (++as == NSA) { as = 0; aph ^= 1; }
+        }
+        tc_commit_pair(d_full);
+      }
+#if SQ_PRE_TRACE
+      tr[3] = clock64() - t_all;
+      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + i] = tr[i];
+#endif
+    }
+  } else if (warp >= kDequantWarp0) {
+    // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
+    const int q = (warp - kDequantWarp0) % 4;   // TMEM sub-partition (warp % 4)
+    const int ch = (warp - kDequantWarp0) / 4;  // column split among warps of one quarter
+    const int row = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int cs = 0, as = 0;
+    uint32_t cph = 0, aph = 0, dph = 0;
+#if SQ_PRE_TRACE
+    unsigned long long tr[4] = {0, 0, 0, 0};
+#endif
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      const int n0 = (tile / m_tiles) * 2 * BM + (int)rank * BM;
+      const int m0 = (tile % m_tiles) * BT2;
+      for (int g = 0; g < G; ++g) {
+        PTW(0, mbar_wait(c_full(cs), cph));
+        const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
+        const int sw = (row >> 1) & 3;
+        // this warp's 16-byte chunks of the group row: k-block h uses chunks 2h .. 2h+1,
+        // split across the kColSplit warps of this lane quarter
+        constexpr int kCh = 4 / kColSplit;
+        uint4 cv[kCh];
+#pragma unroll
+        for (int c = 0; c < kCh; ++c) {
+          const int cc = (c / (2 / kColSplit)) * 2 + (kColSplit == 2 ? ch : (c % 2));
+          cv[c] = *reinterpret_cast<const uint4*>(crow + ((cc ^ sw) << 4));
+        }
+        const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
+        const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(c_empty(cs));
+        if (++cs == NSC) { cs = 0; cph ^= 1; }
+        const __half zh = __ushort_as_half(zbits);
+        const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), zh));
+        const __half2 d2h = __half2half2(__ushort_as_half(sbits));
+        const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
+        const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
+        const float df = __half2float(__ushort_as_half(sbits));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          constexpr int kW = 8 / kColSplit;
+          uint32_t words[kW];
+#pragma unroll
+          for (int c = 0; c < kW / 4; ++c) {
+            const uint4 v = cv[h * (kW / 4) + c];
+            words[4 * c] = v.x; words[4 * c + 1] = v.y; words[4 * c + 2] = v.z; words[4 * c + 3] = v.w;
+          }
+          uint32_t a[4 * kW];
+#pragma unroll
+          for (int wd = 0; wd < kW; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+          PTW(1, mbar_wait(a_empty(as), aph ^ 1));
+          tc_fence_after();
+          if constexpr (kColSplit == 1)
+            tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2),
+                               *reinterpret_cast<const uint32_t(*)[32]>(a));
+          else
+            tmem_st_32x32b_x16(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2) + ch * 16, a);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(a_full(as));
+          if (++as == NSA) { as = 0; aph ^= 1; }
+        }
+      }
+      // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
+      pdl_wait();
+      PTW(2, mbar_wait(d_full, dph));
+      dph ^= 1;
+#if SQ_PRE_TRACE
+      const long long t_ep = clock64();
+#endif
+      tc_fence_after();
+      const int n = n0 + row;
+      const int mt = min(BT2, M - m0);
+      // warps sharing a lane quarter take alternating 16-token column blocks
+      for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
+        tmem_ld_wait();
+        if (n < N) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (c0 + i < mt) {
+              const float f = __uint_as_float(v[i]);
+              Y[(size_t)(m0 + c0 + i) * N + n] = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
+                                                       : __half_as_ushort(__float2half_rn(f));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(d_empty);
+#if SQ_PRE_TRACE
+      tr[3] += clock64() - t_ep;
+#endif
+    }
+#if SQ_PRE_TRACE
+    if (warp == kDequantWarp0 && lane == 0)
+      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + 4 + i] = tr[i];
+#endif
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // the peer's MMAs may still read this CTA's TMEM / SMEM until here
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
                  "r"(TMEM_COLS));
   }
 }
@@ -433,8 +885,9 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
                            cudaStream_t st, const char** why) {
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = K / kGroup;
+  const bool pair = SQ_PRE_2CTA != 0;
   bool ok = encode_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_UINT16, X, (uint64_t)K, (uint64_t)M,
-                      (uint64_t)K * 2, BK, BT, CU_TENSOR_MAP_SWIZZLE_128B);
+                      (uint64_t)K * 2, BK, pair ? p2::BT2 / 2 : BT, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
                        (uint64_t)K / 2, kGroup / 2, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G,
@@ -445,19 +898,42 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
     *why = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
-  const int num_tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
-  const int grid = std::min(num_tiles, num_sms());
-  cudaError_t e;
-  if (x_dtype == SQ_BF16) {
-    e = cudaFuncSetAttribute(prefill_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
-    if (e != cudaSuccess) return e;
-    prefill_kernel<true><<<grid, kThreads, SMEM_ALLOC, st>>>(tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K);
-  } else {
-    e = cudaFuncSetAttribute(prefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
-    if (e != cudaSuccess) return e;
-    prefill_kernel<false><<<grid, kThreads, SMEM_ALLOC, st>>>(tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K);
-  }
+  const int num_tiles = pair ? ((N + 2 * BM - 1) / (2 * BM)) * ((M + p2::BT2 - 1) / p2::BT2)
+                            : ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int grid = pair ? 2 * std::min(num_tiles, num_sms() / 2) : std::min(num_tiles, num_sms());
+  auto kern = pair ? (x_dtype == SQ_BF16 ? prefill2_kernel<true> : prefill2_kernel<false>)
+                   : (x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>);
+  const int smem = pair ? p2::SMEM_ALLOC : SMEM_ALLOC;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = option(SQ_OPT_PDL) ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = pair ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
+  e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 }  // namespace sq
+
+#if SQ_PRE_TRACE
+// development hook: copy the per-CTA wait-cycle trace of the last prefill launch
+extern "C" __attribute__((visibility("default"))) int sq_debug_prefill_trace(void* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, sq::g_pre_trace, sizeof(unsigned long long) * (size_t)n);
+}
+extern "C" __attribute__((visibility("default"))) int sq_debug_prefill_timeline(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, sq::g_pre_ts, sizeof(long long) * 16 * 1024);
+}
+#endif

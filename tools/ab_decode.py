@@ -25,20 +25,24 @@ def bind(path):
 
 
 def main():
-    libs = [(os.path.basename(p), bind(p)) for p in sys.argv[1:]]
+    args = sys.argv[1:]
+    path, ms = 1, (1, 16)
+    if args and args[0] == "--prefill":
+        path, ms, args = 2, (2048,), args[1:]
+    libs = [(os.path.basename(p), bind(p)) for p in args]
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    launches = 48
+    launches = 48 if "--prefill" not in sys.argv else 8
     res = {}
     for name, (K, N) in SHAPES.items():
         wb = K * N // 2 + 4 * N * K // 128
-        copies = max(2, (4 * l2) // wb + 1)
+        copies = max(2, (4 * l2) // wb + 1) if "--prefill" not in sys.argv else 2
         W = (torch.randn(N, K, device=dev) * 0.02).half()
         q0 = sq.quantize_pack_groupwise(W)
         del W
         qs = [q0] + [sq.QuantizedLinear(q0.Wq.clone(), q0.scales.clone(), q0.zeros.clone(), N, K)
                      for _ in range(copies - 1)]
-        for M in (1, 16):
+        for M in ms:
             x = torch.randn(M, K, device=dev).half()
             y = torch.empty(M, N, device=dev, dtype=torch.half)
             graphs = []
@@ -49,7 +53,7 @@ def main():
                 def call(q, L=L, ws=ws, nb=nb):
                     st = L.sq_w4a16_gemm_path(x.data_ptr(), 0, q.Wq.data_ptr(), q.scales.data_ptr(),
                                               q.zeros.data_ptr(), y.data_ptr(), M, N, K, 128, ws.data_ptr(),
-                                              nb + 256, 1, torch.cuda.current_stream().cuda_stream)
+                                              nb + 256, path, torch.cuda.current_stream().cuda_stream)
                     assert st == 0, st
                 for q in qs:
                     call(q)
@@ -71,6 +75,8 @@ def main():
                     torch.cuda.synchronize()
                     times[lname].append(e0.elapsed_time(e1) * 1e3 / launches)
             B = wb + 2 * M * K + 2 * M * N
+            if path == 2:
+                B = 2 * M * N * K * 6532.2 / 1657.7  # report the fraction of the dense fp16 peak
             row = {"shape": name, "M": M}
             for ln, ts in times.items():
                 ts = sorted(ts)[1:-1]

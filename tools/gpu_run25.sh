@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python tools/ab_decode.py paper_2312_03788_b200/_lib/variants/libsq_base.so paper_2312_03788_b200/_lib/variants/libsq_c3ns2.so paper_2312_03788_b200/_lib/variants/libsq_c2ns3.so > gpurun_out/ab.log 2>&1
+echo "ab exit $?" >> gpurun_out/status.txt
