@@ -73,8 +73,16 @@ enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
  *  SQ_OPT_WEIGHTS_STATIC (default 0): the caller promises that Wq/scales/zeros
  *    are not written by the kernels that immediately precede a GEMM on its
  *    stream (true for inference with resident weights).  The decode kernel then
- *    streams its first weight stages BEFORE waiting on the previous kernel. */
-enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2 };
+ *    streams its first weight stages BEFORE waiting on the previous kernel.
+ *  SQ_OPT_DECODE_SCHEDULE (default SQ_SCHED_AUTO): how the decode kernel splits
+ *    the weight matrix over its persistent CTAs.  SQ_SCHED_STREAMK: equal
+ *    contiguous ranges of (row block x 4 groups) units, row blocks cut between
+ *    CTAs finished by a deterministic fixup through the workspace.
+ *    SQ_SCHED_ROWBLOCK: whole row blocks (32 or 64 rows) per CTA, no fixup.
+ *    AUTO takes ROWBLOCK when its wave quantization keeps >= 85 % of the CTAs
+ *    busy, STREAMK otherwise.  Results agree to fp32 rounding either way. */
+enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2, SQ_OPT_DECODE_SCHEDULE = 3 };
+enum { SQ_SCHED_AUTO = 0, SQ_SCHED_STREAMK = 1, SQ_SCHED_ROWBLOCK = 2 };
 
 /* Library version (major*10000 + minor*100 + patch). */
 SQ_API int sq_version(void);
@@ -139,9 +147,10 @@ SQ_API sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const fl
 
 /*
  * Bytes of caller-allocated device workspace sq_w4a16_gemm needs for this shape
- * (the decode path's stream-K fixup: per-row-block counters + fp32 partial tiles).
- * The workspace must be 16-byte aligned and zero-filled once before its first
- * use; every call leaves it zero-filled again.  Calls that may run concurrently
+ * (the decode path's stream-K fixup: fp32 partial tiles, then per-row-block
+ * counters).  The workspace must be 16-byte aligned and zero-filled once before
+ * its first use; every call leaves the counters zero again, so one workspace can
+ * serve any sequence of shapes on one stream.  Calls that may run concurrently
  * (different streams) need different workspaces.
  */
 SQ_API size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group);

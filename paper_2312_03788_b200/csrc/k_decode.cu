@@ -4,21 +4,25 @@
 //   PAPER.md:104-106 Eq. 3 with Ŵ of Eq. 1 line 2; fp32 accumulation.
 //
 // Design:
-//  * Persistent stream-K: the (64-row block x 4-group stage) units of the whole GEMM
-//    are split into equal contiguous ranges, one per resident CTA (one wave, no
-//    tail); a row block cut between CTAs is finished by a deterministic fixup (the
-//    last contributor sums the fp32 partials in CTA order).
-//  * One producer warp streams each unit with TMA into a 4-stage SMEM ring: packed
-//    codes (3-D box 64 B x 64 rows x 4 groups), the scale/zero rows and the matching
-//    X slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free) --
-//    about 100 KB per SM in flight, which is what HBM's latency-bandwidth product
-//    asks for.
-//  * Four consumer warps: warp w takes group w of every stage for all 64 rows (4
-//    row tiles of 16), so its X fragment is loaded (and k-permuted with PRMT) once
-//    and reused four times.  Codes are turned into the EXACT integer (q - Z) in
-//    fp16/bf16 with the lop3 magic-number trick and fed to mma.sync.m16n8k16 with
-//    fp32 accumulation; Δ is applied once per group to the accumulator fragment.
-//  * Row-block results of the 4 consumer warps are summed through shared memory.
+//  * Persistent kernel, one wave of resident CTAs.  The weight matrix is cut into
+//    units of (BN-row block x 4 groups).  Two schedules (SQ_OPT_DECODE_SCHEDULE):
+//    stream-K (equal contiguous unit ranges per CTA; a row block cut between CTAs is
+//    finished by a deterministic fixup: the last contributor sums the fp32 partials
+//    in CTA order) and row-block (whole 32- or 64-row blocks per CTA, no fixup),
+//    chosen per shape by wave quantization.
+//  * One producer warp streams each unit with TMA into an SMEM ring: packed codes
+//    (3-D box 64 B x BN rows x 4 groups), the scale/zero rows and the matching X
+//    slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free).
+//  * Four consumer warps: warp w takes group w of every stage for all BN rows, so
+//    its X fragment is loaded (and k-permuted with PRMT) once and reused BN/16
+//    times.  Codes are turned into the EXACT integer (q - Z) in fp16/bf16 with the
+//    lop3 magic-number trick and fed to mma.sync.m16n8k16 with fp32 accumulation;
+//    Δ is applied once per group to the accumulator fragment.
+//  * At the end of a row-block segment the consumer warps park their fp32 partial
+//    sums in SMEM (over their own, already consumed, activation slice of the stage)
+//    and go on; a sixth warp (epilogue) sums the four in fixed order, hands the stage
+//    back to the producer and does the global work (Y store or stream-K fixup) off
+//    the consumers' critical path.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,66 +36,42 @@ namespace sq {
 namespace {
 
 constexpr int kGroup = 128;
-#ifndef SQ_DEC_BN
-#define SQ_DEC_BN 64
-#endif
 #ifndef SQ_DEC_CTAS
 #define SQ_DEC_CTAS 2
 #endif
-#ifndef SQ_DEC_NS1
-#define SQ_DEC_NS1 4
-#endif
-#ifndef SQ_DEC_NS2
-#define SQ_DEC_NS2 3
-#endif
-#ifndef SQ_DEC_ROWMAJOR
-#define SQ_DEC_ROWMAJOR 0  // 1: codes box traversed row by row (256 contiguous bytes per row)
-#endif
-#ifndef SQ_DEC_NOLOAD
-#define SQ_DEC_NOLOAD 0  // experiment: after the first NS stages, recompute on resident data (compute ceiling)
-#endif
-#ifndef SQ_DEC_NOCOMPUTE
-#define SQ_DEC_NOCOMPUTE 0  // experiment: stream the operands but skip the math (bandwidth ceiling)
+#ifndef SQ_DEC_SX
+#define SQ_DEC_SX 0  // 1: magic-offset codes straight into the MMA + activation-sum correction
 #endif
 #ifndef SQ_DEC_ABLATE
-#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant (wrong results)
+#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue
 #endif
-#ifndef SQ_DEC_CHAINS
-#define SQ_DEC_CHAINS 1  // independent MMA accumulator chains per row tile (1, 2 or 4)
-#endif
-#ifndef SQ_DEC_IL
-#define SQ_DEC_IL 0  // 1: load all 4 row tiles' codes first, then interleave their MMA chains
-#endif
-#ifndef SQ_DEC_SX
-#define SQ_DEC_SX 0  // 1: magic-offset MMAs + activation-sum correction (no per-code hsub/hfma)
-#endif
-#ifndef SQ_DEC_PF
-#define SQ_DEC_PF 0   // L2 prefetch distance in units ahead of the SMEM ring (0 = off)
-#endif
-constexpr int BN = SQ_DEC_BN;   // rows per row block (multiple of 16)
-constexpr int kRT = BN / 16;    // 16-row tiles per consumer warp
-#ifndef SQ_DEC_GPW
-#define SQ_DEC_GPW 1  // groups per consumer warp per stage
-#endif
-constexpr int GPW = SQ_DEC_GPW;
-constexpr int GPS = 4 * GPW;    // groups per stage (4 consumer warps x GPW)
+constexpr int GPS = 4;          // groups per stage = consumer warps
 constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kProducerWarp = kConsumerWarps;      // TMA
+constexpr int kEpilogueWarp = kConsumerWarps + 1;  // cross-warp sum, output / stream-K fixup
+constexpr int kThreads = (kConsumerWarps + 2) * 32;
 constexpr int kMaxCtasPerSm = SQ_DEC_CTAS;
+constexpr int kMaxBN = 64;      // row-block heights: 32 or 64
+constexpr int kMinBN = 32;
+constexpr int kSmemBudget = 112 * 1024;  // per CTA, two CTAs per SM
 
-template <int MT>
+template <int MT, int BN>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
-  static constexpr int NS = MT == 1 ? SQ_DEC_NS1 : SQ_DEC_NS2;
-  static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB
+  static constexpr int RT = BN / 16;                      // 16-row tiles per consumer warp
+  static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
   static constexpr int XB = GPS * MPAD * kGroup * 2;      // 8 / 16 KB
-  static constexpr int SZ = GPS * BN * 2;                 // 512 B
-  static constexpr int STAGE = CODES + XB + 2 * SZ;
-  static constexpr int OFF_RED = NS * STAGE;
-  static constexpr int RED = (kConsumerWarps - 1) * MPAD * BN * 4;
-  static constexpr int OFF_BAR = OFF_RED + RED;
-  static constexpr int OFF_FLAG = OFF_BAR + 2 * NS * 8;
-  static constexpr int SMEM = OFF_FLAG + 16;
+  static constexpr int SZ = GPS * BN * 2;
+  // stage bases stay 1024-B aligned (SWIZZLE_128B destination of the X box)
+  static constexpr int TX = CODES + XB + 2 * SZ;  // bytes the TMA delivers per stage
+  static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
+  static constexpr int NS = std::min(8, (kSmemBudget - 1024 - 256) / STAGE);
+  // At a segment end each consumer warp parks its fp32 partial sums (MPAD x BN) over its
+  // own group's activation slice of the stage, which only that warp reads.
+  static constexpr int XSLICE = XB / GPS;
+  static_assert(MPAD * BN * 4 <= XSLICE, "partial-sum slot must fit the activation slice");
+  static constexpr int OFF_BAR = NS * STAGE;  // full[NS], empty[NS], red_full[NS]
+  static constexpr int SMEM = OFF_BAR + 3 * NS * 8;
   static constexpr int SMEM_ALLOC = SMEM + 1024;
 };
 
@@ -108,6 +88,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(cnt) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -135,19 +118,8 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint3
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n"
-               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2) : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n"
-               ::"l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1) : "memory");
-}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-}
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
@@ -244,12 +216,45 @@ __device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint
   }
 }
 
+// Work split.  Units are numbered u = rb * upb + pos (row block rb, stage pos).
+//  stream-K (dp = 0): CTA c owns the contiguous range [start(c), start(c + 1)).
+//  row-block (dp = 1): CTA c owns row blocks c, c + P, c + 2P, ... (each a full range).
 struct Work {
-  int units, upb, cta_q, cta_r;  // total units, units per row block, units per CTA (q, remainder)
+  int units, upb, cta_q, cta_r, rbs, dp;
   __device__ __forceinline__ int start(int c) const { return c * cta_q + min(c, cta_r); }
   __device__ __forceinline__ int cta_of(int u) const {
     const int big = (cta_q + 1) * cta_r;
     return u < big ? u / (cta_q + 1) : cta_r + (u - big) / cta_q;
+  }
+};
+
+// Walks the units of one CTA in processing order (identical in all three warp roles).
+struct Sched {
+  int c, P, ri, nr, u, ue;
+  __device__ __forceinline__ Sched(const Work& wk, int c_, int P_) : c(c_), P(P_), ri(0) {
+    nr = wk.dp ? (wk.rbs - c + P - 1) / P : 1;
+    load(wk);
+  }
+  __device__ __forceinline__ void load(const Work& wk) {
+    if (ri >= nr) return;
+    if (wk.dp) {
+      u = (c + ri * P) * wk.upb;
+      ue = u + wk.upb;
+    } else {
+      u = wk.start(c);
+      ue = wk.start(c + 1);
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return ri < nr; }
+  __device__ __forceinline__ bool range_start(const Work& wk) const {
+    return wk.dp ? (u % wk.upb == 0) : (u == wk.start(c));
+  }
+  __device__ __forceinline__ bool range_last() const { return u + 1 == ue; }
+  __device__ __forceinline__ void next(const Work& wk) {
+    if (++u == ue) {
+      ++ri;
+      load(wk);
+    }
   }
 };
 
@@ -258,29 +263,28 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-template <int MT, bool kBF16>
+template <int MT, bool kBF16, int BN>
 __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
               int M, int N, Work wk, int early_weights) {
-  using C = Cfg<MT>;
+  using C = Cfg<MT, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + C::OFF_BAR;
   const uint32_t bar_empty = bar_full + 8 * C::NS;
-  int* flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
-  float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
+  const uint32_t red_full = bar_empty + 8 * C::NS;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c = blockIdx.x;
-  const int u0 = wk.start(c), u1 = wk.start(c + 1);
+  const int c = blockIdx.x, P = gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(bar_full + 8 * i, 1);
       mbar_init(bar_empty + 8 * i, kConsumerWarps);
+      mbar_init(red_full + 8 * i, kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -288,83 +292,154 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
   // the next kernel in the stream may start its prologue as our CTAs retire
   pdl_launch_dependents();
 
-  if (warp == kConsumerWarps) {
+  if (warp == kProducerWarp) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       prefetch_tmap(&tm_w);
       prefetch_tmap(&tm_x);
       prefetch_tmap(&tm_s);
       prefetch_tmap(&tm_z);
+      auto load_weights = [&](uint32_t st, uint32_t fb, int u) {
+        const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
+        tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+        tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
+        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+      };
       // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
       // declared them static: stream the first stages before waiting on it.
       int pre = 0;
-      // L2 prefetch cursor, SQ_DEC_PF units ahead of the SMEM ring: more bytes in flight
-      // from HBM than the shared-memory ring alone can hold
-      int pf_u = u0, pf_rb = u0 / wk.upb, pf_g0 = (u0 % wk.upb) * GPS;
-      auto prefetch_next = [&]() {
-        if (SQ_DEC_PF > 0 && pf_u < u1) {
-          if (SQ_DEC_ROWMAJOR) tma_prefetch_3d(&tm_w, 0, pf_g0, pf_rb * BN);
-          else tma_prefetch_3d(&tm_w, 0, pf_rb * BN, pf_g0);
-          tma_prefetch_2d(&tm_s, pf_rb * BN, pf_g0);
-          tma_prefetch_2d(&tm_z, pf_rb * BN, pf_g0);
-          ++pf_u;
-          pf_g0 += GPS;
-          if (pf_g0 >= wk.upb * GPS) { pf_g0 = 0; ++pf_rb; }
-        }
-      };
-      if (SQ_DEC_PF > 0 && early_weights)
-        for (int q = 0; q < C::NS + SQ_DEC_PF; ++q) prefetch_next();
       if (early_weights) {
-        int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
-        for (; pre < C::NS && u0 + pre < u1; ++pre) {
-          const uint32_t st = sbase + pre * C::STAGE;
+        Sched sc(wk, c, P);
+        for (; pre < C::NS && sc.valid(); ++pre, sc.next(wk)) {
           const uint32_t fb = bar_full + 8 * pre;
-          mbar_expect_tx(fb, C::STAGE);
-          if (SQ_DEC_ROWMAJOR) tma_3d(st, &tm_w, fb, 0, g0, rb * BN);
-          else tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
-          tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
-          tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
-          g0 += GPS;
-          if (g0 >= wk.upb * GPS) { g0 = 0; ++rb; }
+          mbar_expect_tx(fb, C::TX);
+          load_weights(sbase + pre * C::STAGE, fb, sc.u);
         }
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
-      if (SQ_DEC_PF > 0 && !early_weights)
-        for (int q = 0; q < C::NS + SQ_DEC_PF; ++q) prefetch_next();
-      int rb = u0 / wk.upb, g0 = (u0 % wk.upb) * GPS;
       int s = 0;
       uint32_t ph = 0;
-      for (int i = 0; u0 + i < u1; ++i) {
+      int i = 0;
+      for (Sched sc(wk, c, P); sc.valid(); sc.next(wk), ++i) {
         const uint32_t st = sbase + s * C::STAGE;
         const uint32_t fb = bar_full + 8 * s;
-        if (i < pre) {
-          tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
-        } else if (SQ_DEC_NOLOAD && i >= C::NS) {
+        if (i >= pre) {
           mbar_wait(bar_empty + 8 * s, ph ^ 1);
-          mbar_arrive(fb);
-        } else {
-          mbar_wait(bar_empty + 8 * s, ph ^ 1);
-          mbar_expect_tx(fb, C::STAGE);
-          if (SQ_DEC_ROWMAJOR) tma_3d(st, &tm_w, fb, 0, g0, rb * BN);
-          else tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
-          tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, g0);
-          tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
-          tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
-          prefetch_next();
+          mbar_expect_tx(fb, C::TX);
+          load_weights(st, fb, sc.u);
         }
+        tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, (sc.u % wk.upb) * GPS);
         if (++s == C::NS) { s = 0; ph ^= 1; }
-        g0 += GPS;
-        if (g0 >= wk.upb * GPS) { g0 = 0; ++rb; }
       }
+    }
+    return;
+  }
+
+  auto to_out = [](float v) -> uint16_t {
+    if (kBF16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    return __half_as_ushort(__float2half_rn(v));
+  };
+
+  if (warp == kEpilogueWarp) {
+    // ===================== epilogue: one warp, off the consumers' critical path =====================
+    // Walks the same schedule as the consumers.  At each segment end it sums the four
+    // warps' parked partials (fixed warp order), hands the stage back to the producer,
+    // then writes Y (whole row block) or runs the stream-K fixup (partial row block).
+    constexpr int E = C::MPAD * BN / 32;  // elements per lane
+    int s = 0;
+    uint32_t redph = 0;                   // phase bit per stage
+    int seg_begin_pos = 0;
+    bool first_seg = true, waited = false;
+    for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
+      const int rb = sc.u / wk.upb, pos = sc.u % wk.upb;
+      if (sc.range_start(wk)) seg_begin_pos = pos;
+      const bool rb_done = pos + 1 == wk.upb;
+      if (rb_done || sc.range_last()) {
+        mbar_wait(red_full + 8 * s, (redph >> s) & 1u);
+        redph ^= 1u << s;
+        const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODES);
+        constexpr int W = C::XSLICE / 4;  // floats per warp slot
+        float v[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int idx = lane + 32 * i;
+          v[i] = ((sl[idx] + sl[W + idx]) + sl[2 * W + idx]) + sl[3 * W + idx];
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(bar_empty + 8 * s, kConsumerWarps);  // stage back to the producer
+        if (!waited) {  // global accesses below must follow the previous kernel (PDL)
+          pdl_wait();
+          waited = true;
+        }
+        const int n0 = rb * BN;
+        if (SQ_DEC_ABLATE == 8) {
+          if (v[0] == 1234.5f) Y[0] = 1;
+        } else if (seg_begin_pos == 0 && rb_done) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+            if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(v[i]);
+          }
+        } else if (SQ_DEC_ABLATE == 16) {
+          if (v[0] == 1234.5f) Y[0] = 1;
+        } else {
+          // stream-K fixup: park the partial; the last contributor sums them in CTA order
+          float* slot = partials + ((size_t)c * 2 + (first_seg ? 0 : 1)) * (16 * kMaxBN);
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const int idx = lane + 32 * i;
+            if (idx < M * BN) __stcg(slot + idx, v[i]);
+          }
+          __syncwarp();
+          const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
+          int last = 0;
+          if (lane == 0) {
+            // acq_rel: publishes this warp's partial (ordered by __syncwarp) and, for the
+            // last contributor, makes the others' partials visible to the loads below
+            int prev;
+            asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;\n"
+                         : "=r"(prev) : "l"(counters + rb) : "memory");
+            last = prev == c1 - c0;
+          }
+          if (__shfl_sync(0xffffffffu, last, 0)) {
+            // sum in fixed CTA order; each CTA's E loads are independent (one L2 round trip per CTA)
+            float tot[E];
+#pragma unroll
+            for (int i = 0; i < E; ++i) tot[i] = 0.0f;
+            for (int cc = c0; cc <= c1; ++cc) {
+              const int e = (wk.start(cc) / wk.upb == rb) ? 0 : 1;
+              const float* src = partials + ((size_t)cc * 2 + e) * (16 * kMaxBN);
+              float part[E];
+#pragma unroll
+              for (int i = 0; i < E; ++i) {
+                const int idx = lane + 32 * i;
+                part[i] = idx < M * BN ? __ldcg(src + idx) : 0.0f;
+              }
+#pragma unroll
+              for (int i = 0; i < E; ++i) tot[i] += part[i];
+            }
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+              const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+              if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(tot[i]);
+            }
+            if (lane == 0) counters[rb] = 0;  // leave the workspace zeroed
+          }
+        }
+        first_seg = false;
+        seg_begin_pos = 0;
+      }
+      if (++s == C::NS) s = 0;
     }
     return;
   }
 
   // ===================== consumers: warp w = group w of each stage =====================
   const int r = lane / 4, j = lane % 4;
-  float acc[kRT][MT][4];
+  float acc[C::RT][MT][4];
 #pragma unroll
-  for (int rt = 0; rt < kRT; ++rt)
+  for (int rt = 0; rt < C::RT; ++rt)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -372,28 +447,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   int s = 0;
   uint32_t ph = 0;
-  int rb = u0 / wk.upb;            // current row block
-  int pos = u0 - rb * wk.upb;      // unit index inside the row block
-  int seg_begin_pos = pos;
-  bool first_seg = true;
-  bool waited = false;
-  for (int u = u0; u < u1; ++u) {
+  for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
     mbar_wait(bar_full + 8 * s, ph);
     const uint32_t st = sbase + s * C::STAGE;
-#if SQ_DEC_NOCOMPUTE
-    if (true) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
-      if (++s == C::NS) { s = 0; ph ^= 1; }
-      ++pos;
-      if (pos == wk.upb) { ++rb; pos = 0; seg_begin_pos = 0; first_seg = false; }
-      continue;
-    }
-#endif
-
-#pragma unroll
-    for (int gi = 0; gi < GPW; ++gi) {
-    const int grp = warp + kConsumerWarps * gi;  // group of the stage this pass works on
+    const int grp = warp;
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
 #pragma unroll
@@ -414,10 +471,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         xb[mt][w][3] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x7632u);  // (x3, x7)
       }
     }
-#if SQ_DEC_SX
-    // activation sums of this group for this lane's tokens: even-k and odd-k positions
+    // activation sums of this group for this lane's tokens, even-k and odd-k positions
+    // (SQ_DEC_SX: the MMAs see 1024 + q, the zero point and offset are removed per group)
     float sxe[MT][2], sxo[MT][2];
-    {
+    if (SQ_DEC_SX) {
       const uint32_t kOnes = kBF16 ? 0x3F803F80u : 0x3C003C00u;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -433,94 +490,45 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         sxo[mt][0] = so[0]; sxo[mt][1] = so[1];
       }
     }
-#endif
-    // codes of this warp's group: [group][row][64 B] (default) or [row][group][64 B]
-    const uint32_t cbase = SQ_DEC_ROWMAJOR ? st + grp * 64 + r * (GPS * 64) + j * 16
-                                           : st + grp * (BN * 64) + r * 64 + j * 16;
-    constexpr int kRowStride = SQ_DEC_ROWMAJOR ? GPS * 64 : 64;
+    // codes of this warp's group: [group][row][64 B]
+    const uint32_t cbase = st + grp * (BN * 64) + r * 64 + j * 16;
     const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
     const uint32_t sbz = sbs + C::SZ;
-#if SQ_DEC_IL
-    {
-      uint32_t wa[kRT][4], wb[kRT][4], zsA[kRT], zfA[kRT], zsB[kRT], zfB[kRT];
-      float dA[kRT], dB[kRT];
 #pragma unroll
-      for (int rt = 0; rt < kRT; ++rt) {
-        const uint4 ca = lds128(cbase + rt * 16 * kRowStride);
-        const uint4 cb = lds128(cbase + (rt * 16 + 8) * kRowStride);
-        wa[rt][0] = ca.x; wa[rt][1] = ca.y; wa[rt][2] = ca.z; wa[rt][3] = ca.w;
-        wb[rt][0] = cb.x; wb[rt][1] = cb.y; wb[rt][2] = cb.z; wb[rt][3] = cb.w;
-        dA[rt] = __half2float(__ushort_as_half(lds16(sbs + rt * 32)));
-        dB[rt] = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
-        zero_consts<kBF16>(lds16(sbz + rt * 32), zsA[rt], zfA[rt]);
-        zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB[rt], zfB[rt]);
-      }
-      float g[kRT][MT][4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-#pragma unroll
-        for (int rt = 0; rt < kRT; ++rt) {
-          uint32_t hA[4], hB[4];
-          dequant_word<kBF16>(wa[rt][w], zsA[rt], zfA[rt], hA);
-          dequant_word<kBF16>(wb[rt][w], zsB[rt], zfB[rt], hB);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            if (w == 0) {
-              mma_16816_zc(g[rt][mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
-            } else {
-              mma_16816(g[rt][mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
-            }
-            mma_16816(g[rt][mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
-          }
-        }
-      }
-#pragma unroll
-      for (int rt = 0; rt < kRT; ++rt)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          acc[rt][mt][0] = fmaf(g[rt][mt][0], dA[rt], acc[rt][mt][0]);
-          acc[rt][mt][1] = fmaf(g[rt][mt][1], dA[rt], acc[rt][mt][1]);
-          acc[rt][mt][2] = fmaf(g[rt][mt][2], dB[rt], acc[rt][mt][2]);
-          acc[rt][mt][3] = fmaf(g[rt][mt][3], dB[rt], acc[rt][mt][3]);
-        }
-    }
-    if (false)
-#endif
-#pragma unroll
-    for (int rt = 0; rt < kRT; ++rt) {
-      const uint4 ca = lds128(cbase + rt * 16 * kRowStride);
-      const uint4 cb = lds128(cbase + (rt * 16 + 8) * kRowStride);
+    for (int rt = 0; rt < C::RT; ++rt) {
+      const uint4 ca = lds128(cbase + rt * 16 * 64);
+      const uint4 cb = lds128(cbase + (rt * 16 + 8) * 64);
       const float dA = __half2float(__ushort_as_half(lds16(sbs + rt * 32)));
       const float dB = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
-#if SQ_DEC_SX
-      {
+      const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
+      const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+      if (SQ_DEC_SX) {
         const float zA = __half2float(__ushort_as_half(lds16(sbz + rt * 32)));
         const float zB = __half2float(__ushort_as_half(lds16(sbz + rt * 32 + 16)));
-        const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
-        const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+        constexpr uint32_t kMagic = kBF16 ? 0x43004300u : 0x64006400u;
         float ge[MT][4], go[MT][4];
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t la0, la1, ha0, ha1, lb0, lb1, hb0, hb1;
-          if (!kBF16) {
+          if (!kBF16) {  // 1024 + q for the low nibbles, 1024 + 16 q for the high ones
             const uint32_t ta = wa[w] >> 8, tb = wb[w] >> 8;
-            la0 = lop3_and_or(wa[w], 0x000F000Fu, 0x64006400u);  // 1024 + (e0, e4)
-            la1 = lop3_and_or(ta, 0x000F000Fu, 0x64006400u);     // 1024 + (e2, e6)
-            ha0 = lop3_and_or(wa[w], 0x00F000F0u, 0x64006400u);  // 1024 + 16 (e1, e5)
-            ha1 = lop3_and_or(ta, 0x00F000F0u, 0x64006400u);     // 1024 + 16 (e3, e7)
-            lb0 = lop3_and_or(wb[w], 0x000F000Fu, 0x64006400u);
-            lb1 = lop3_and_or(tb, 0x000F000Fu, 0x64006400u);
-            hb0 = lop3_and_or(wb[w], 0x00F000F0u, 0x64006400u);
-            hb1 = lop3_and_or(tb, 0x00F000F0u, 0x64006400u);
-          } else {
-            la0 = lop3_and_or(wa[w], 0x000F000Fu, 0x43004300u);
-            la1 = lop3_and_or(wa[w] >> 8, 0x000F000Fu, 0x43004300u);
-            ha0 = lop3_and_or(wa[w] >> 4, 0x000F000Fu, 0x43004300u);
-            ha1 = lop3_and_or(wa[w] >> 12, 0x000F000Fu, 0x43004300u);
-            lb0 = lop3_and_or(wb[w], 0x000F000Fu, 0x43004300u);
-            lb1 = lop3_and_or(wb[w] >> 8, 0x000F000Fu, 0x43004300u);
-            hb0 = lop3_and_or(wb[w] >> 4, 0x000F000Fu, 0x43004300u);
-            hb1 = lop3_and_or(wb[w] >> 12, 0x000F000Fu, 0x43004300u);
+            la0 = lop3_and_or(wa[w], 0x000F000Fu, kMagic);
+            la1 = lop3_and_or(ta, 0x000F000Fu, kMagic);
+            ha0 = lop3_and_or(wa[w], 0x00F000F0u, kMagic);
+            ha1 = lop3_and_or(ta, 0x00F000F0u, kMagic);
+            lb0 = lop3_and_or(wb[w], 0x000F000Fu, kMagic);
+            lb1 = lop3_and_or(tb, 0x000F000Fu, kMagic);
+            hb0 = lop3_and_or(wb[w], 0x00F000F0u, kMagic);
+            hb1 = lop3_and_or(tb, 0x00F000F0u, kMagic);
+          } else {       // 128 + q (bf16 has too few mantissa bits for 128 + 16 q)
+            la0 = lop3_and_or(wa[w], 0x000F000Fu, kMagic);
+            la1 = lop3_and_or(wa[w] >> 8, 0x000F000Fu, kMagic);
+            ha0 = lop3_and_or(wa[w] >> 4, 0x000F000Fu, kMagic);
+            ha1 = lop3_and_or(wa[w] >> 12, 0x000F000Fu, kMagic);
+            lb0 = lop3_and_or(wb[w], 0x000F000Fu, kMagic);
+            lb1 = lop3_and_or(wb[w] >> 8, 0x000F000Fu, kMagic);
+            hb0 = lop3_and_or(wb[w] >> 4, 0x000F000Fu, kMagic);
+            hb1 = lop3_and_or(wb[w] >> 12, 0x000F000Fu, kMagic);
           }
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
@@ -539,7 +547,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const float ceA = -((kBF16 ? 128.0f : 1024.0f) + zA), coA = -((kBF16 ? 128.0f : 64.0f) + zA);
         const float ceB = -((kBF16 ? 128.0f : 1024.0f) + zB), coB = -((kBF16 ? 128.0f : 64.0f) + zB);
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float ce = i < 2 ? ceA : ceB, co = i < 2 ? coA : coB, d = i < 2 ? dA : dB;
@@ -548,61 +556,39 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
             v = fmaf(co, sxo[mt][i & 1], v);
             acc[rt][mt][i] = fmaf(v, d, acc[rt][mt][i]);
           }
-        }
         continue;
       }
-#endif
       uint32_t zsA, zfA, zsB, zfB;
       zero_consts<kBF16>(lds16(sbz + rt * 32), zsA, zfA);
       zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB, zfB);
-      const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
-      const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
-      constexpr int NC = SQ_DEC_CHAINS;
-      float gc[MT][NC][4];
+      float g[MT][4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t hA[4], hB[4];
-#if SQ_DEC_ABLATE == 2
-        hA[0] = wa[w]; hA[1] = wa[w] >> 8; hA[2] = wa[w] >> 4; hA[3] = wa[w] >> 12;
-        hB[0] = wb[w]; hB[1] = wb[w] >> 8; hB[2] = wb[w] >> 4; hB[3] = wb[w] >> 12;
-#else
-        dequant_word<kBF16>(wa[w], zsA, zfA, hA);
-        dequant_word<kBF16>(wb[w], zsB, zfB, hB);
-#endif
-#if SQ_DEC_ABLATE == 1
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            gc[mt][0][i] = (w == 0 ? 0.0f : gc[mt][0][i]) +
-                           __uint_as_float((hA[i] ^ hB[i] ^ xb[mt][w][i]) & 0x3FFFFFFFu);
-        if (false)
-#endif
+        if (SQ_DEC_ABLATE == 2) {
+          hA[0] = wa[w]; hA[1] = wa[w] >> 8; hA[2] = wa[w] >> 4; hA[3] = wa[w] >> 12;
+          hB[0] = wb[w]; hB[1] = wb[w] >> 8; hB[2] = wb[w] >> 4; hB[3] = wb[w] >> 12;
+        } else {
+          dequant_word<kBF16>(wa[w], zsA, zfA, hA);
+          dequant_word<kBF16>(wb[w], zsB, zfB, hB);
+        }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
+          if (SQ_DEC_ABLATE == 1) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int q = 2 * w + h, ch = q % NC;  // q-th MMA of the group -> chain ch
-            if (q < NC) {
-              mma_16816_zc(gc[mt][ch], hA[2 * h], hB[2 * h], hA[2 * h + 1], hB[2 * h + 1],
-                           xb[mt][w][2 * h], xb[mt][w][2 * h + 1], kBF16);
-            } else {
-              mma_16816(gc[mt][ch], hA[2 * h], hB[2 * h], hA[2 * h + 1], hB[2 * h + 1],
-                        xb[mt][w][2 * h], xb[mt][w][2 * h + 1], kBF16);
-            }
+            for (int i = 0; i < 4; ++i)
+              g[mt][i] = (w == 0 ? 0.0f : g[mt][i]) +
+                         __uint_as_float((hA[i] ^ hB[i] ^ xb[mt][w][i]) & 0x3FFFFFFFu);
+            continue;
           }
+          // A = rows (r, r+8) x k pairs; B = the same k pairs of this lane's token
+          if (w == 0)
+            mma_16816_zc(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+          else
+            mma_16816(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+          mma_16816(g[mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
         }
       }
-      float g[MT][4];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float v = gc[mt][0][i];
-#pragma unroll
-          for (int ch = 1; ch < NC; ++ch) v += gc[mt][ch][i];
-          g[mt][i] = v;
-        }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         acc[rt][mt][0] = fmaf(g[mt][0], dA, acc[rt][mt][0]);
@@ -611,117 +597,35 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         acc[rt][mt][3] = fmaf(g[mt][3], dB, acc[rt][mt][3]);
       }
     }
-    }
+
+    // ---- end of a row-block segment?
+    const bool seg_end = (sc.u % wk.upb) + 1 == wk.upb || sc.range_last();
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar_empty + 8 * s);
-    if (++s == C::NS) { s = 0; ph ^= 1; }
-
-    // ---- end of this CTA's segment of row block rb?
-    ++pos;
-    const bool rb_done = pos == wk.upb;
-    if (!rb_done && u + 1 != u1) continue;
-
-    if (!waited) {  // global writes below must follow the previous kernel (PDL)
-      pdl_wait();
-      waited = true;
-    }
-    // sum the 4 consumer warps through shared memory: warps 1..3 park, warp 0 adds
-    if (warp > 0) {
-      float* rw = red + (warp - 1) * C::MPAD * BN;
-#pragma unroll
-      for (int rt = 0; rt < kRT; ++rt)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
-          rw[t0 * BN + ra] = acc[rt][mt][0];
-          rw[(t0 + 1) * BN + ra] = acc[rt][mt][1];
-          rw[t0 * BN + ra + 8] = acc[rt][mt][2];
-          rw[(t0 + 1) * BN + ra + 8] = acc[rt][mt][3];
-        }
-    }
-    consumer_sync();
-    if (warp == 0) {
-#pragma unroll
-      for (int rt = 0; rt < kRT; ++rt)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
-          float v[4] = {acc[rt][mt][0], acc[rt][mt][1], acc[rt][mt][2], acc[rt][mt][3]};
-#pragma unroll
-          for (int w = 0; w < kConsumerWarps - 1; ++w) {
-            const float* rw = red + w * C::MPAD * BN;
-            v[0] += rw[t0 * BN + ra];
-            v[1] += rw[(t0 + 1) * BN + ra];
-            v[2] += rw[t0 * BN + ra + 8];
-            v[3] += rw[(t0 + 1) * BN + ra + 8];
-          }
-          red[t0 * BN + ra] = v[0];  // total parked in slot 0 (each lane owns its entries)
-          red[(t0 + 1) * BN + ra] = v[1];
-          red[t0 * BN + ra + 8] = v[2];
-          red[(t0 + 1) * BN + ra + 8] = v[3];
-        }
-    }
-    consumer_sync();
-#pragma unroll
-    for (int rt = 0; rt < kRT; ++rt)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
-
-    const int n0 = rb * BN;
-    const bool full = (seg_begin_pos == 0) && rb_done;
-    auto to_out = [](float v) -> uint16_t {
-      if (kBF16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
-      return __half_as_ushort(__float2half_rn(v));
-    };
-    if (full) {
-      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) {
-        const int t = idx / BN, row = idx % BN;
-        if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(red[t * BN + row]);
-      }
+    if (!seg_end) {
+      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
     } else {
-      // stream-K fixup: park the partial; the last contributor sums them in CTA order
-      const int e = first_seg ? 0 : 1;
-      float* slot = partials + ((size_t)c * 2 + e) * (16 * BN);
-      for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) __stcg(slot + idx, red[idx]);
-      consumer_sync();
-      const int c0 = wk.cta_of(rb * wk.upb), c1 = wk.cta_of((rb + 1) * wk.upb - 1);
-      if (threadIdx.x == 0) {
-        __threadfence();
-        const int prev = atomicAdd(counters + rb, 1);
-        __threadfence();
-        *flag = (prev == c1 - c0) ? 1 : 0;
-      }
-      consumer_sync();
-      if (*flag) {
-        for (int idx = threadIdx.x; idx < M * BN; idx += kConsumerWarps * 32) {
-          float part[8];
-          float v = 0.0f;
-          int cc = c0;
-          while (cc <= c1) {  // batch the L2 reads, add in fixed CTA order
-            const int nb = min(8, c1 - cc + 1);
+      // park this warp's partial sums over its own activation slice of the stage and hand
+      // them to the epilogue warp, which also releases the stage; no CTA-wide barrier
+      float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::CODES + warp * C::XSLICE);
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (q < nb) {
-                const int ee = (wk.start(cc + q) / wk.upb == rb) ? 0 : 1;
-                part[q] = __ldcg(partials + ((size_t)(cc + q) * 2 + ee) * (16 * BN) + idx);
-              }
+      for (int rt = 0; rt < C::RT; ++rt)
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (q < nb) v += part[q];
-            cc += nb;
-          }
-          const int t = idx / BN, row = idx % BN;
-          if (n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(v);
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
+          slot[t0 * BN + ra] = acc[rt][mt][0];
+          slot[(t0 + 1) * BN + ra] = acc[rt][mt][1];
+          slot[t0 * BN + ra + 8] = acc[rt][mt][2];
+          slot[(t0 + 1) * BN + ra + 8] = acc[rt][mt][3];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
         }
-        if (threadIdx.x == 0) counters[rb] = 0;  // leave the workspace zeroed
-      }
+      // the stage is refilled by TMA (async proxy) after the epilogue releases it: order
+      // these generic-proxy writes before that
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(red_full + 8 * s);
     }
-    consumer_sync();  // red[] and flag are reused by the next segment
-    first_seg = false;
-    if (rb_done) { ++rb; pos = 0; }
-    seg_begin_pos = pos;
+    if (++s == C::NS) { s = 0; ph ^= 1; }
   }
 }
 
@@ -751,31 +655,31 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MT, bool kBF16>
+template <int MT, bool kBF16, int BN>
 int ctas_per_sm() {
   static int cached = -1;
   if (cached < 0) {
     int n = 0;
-    cudaFuncSetAttribute(decode_kernel<MT, kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<MT>::SMEM_ALLOC);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16>, kThreads,
-                                                      Cfg<MT>::SMEM_ALLOC) != cudaSuccess || n < 1)
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<MT, BN>::SMEM_ALLOC);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN>, kThreads,
+                                                      Cfg<MT, BN>::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
     cached = std::min(n, kMaxCtasPerSm);
   }
   return cached;
 }
 
-template <int MT, bool kBF16>
+template <int MT, bool kBF16, int BN>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                     void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
-  using C = Cfg<MT>;
+                     void* Y, int M, int N, int K, void* ws, bool dp, cudaStream_t st, const char** why) {
+  using C = Cfg<MT, BN>;
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
   {
-    const uint64_t d[3] = {64, SQ_DEC_ROWMAJOR ? (uint64_t)G : (uint64_t)N, SQ_DEC_ROWMAJOR ? (uint64_t)N : (uint64_t)G};
-    const uint64_t s[2] = {SQ_DEC_ROWMAJOR ? 64 : (uint64_t)K / 2, SQ_DEC_ROWMAJOR ? (uint64_t)K / 2 : 64};
-    const uint32_t b[3] = {64, SQ_DEC_ROWMAJOR ? (uint32_t)GPS : (uint32_t)BN, SQ_DEC_ROWMAJOR ? (uint32_t)BN : (uint32_t)GPS};
+    const uint64_t d[3] = {64, (uint64_t)N, (uint64_t)G};
+    const uint64_t s[2] = {(uint64_t)K / 2, 64};
+    const uint32_t b[3] = {64, (uint32_t)BN, (uint32_t)GPS};
     if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, Wq, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
       *why = "tensor map (codes)";
       return cudaErrorInvalidValue;
@@ -793,22 +697,26 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   {
     const uint64_t d[2] = {(uint64_t)N, (uint64_t)G};
     const uint64_t s[1] = {(uint64_t)N * 2};
-    const uint32_t b[2] = {BN, GPS};
+    const uint32_t b[2] = {(uint32_t)BN, GPS};
     if (!encode(&ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, scales, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, zeros, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
       *why = "tensor map (scales/zeros)";
       return cudaErrorInvalidValue;
     }
   }
-  const int RB = (N + BN - 1) / BN;
   Work wk;
+  wk.rbs = (N + BN - 1) / BN;
   wk.upb = (G + GPS - 1) / GPS;
-  wk.units = RB * wk.upb;
-  const int P = std::min(wk.units, num_sms() * ctas_per_sm<MT, kBF16>());
+  wk.units = wk.rbs * wk.upb;
+  wk.dp = dp ? 1 : 0;
+  const int slots = num_sms() * ctas_per_sm<MT, kBF16, BN>();
+  const int P = dp ? std::min(wk.rbs, slots) : std::min(wk.units, slots);
   wk.cta_q = wk.units / P;
   wk.cta_r = wk.units % P;
-  int* counters = reinterpret_cast<int*>(ws);
-  float* partials = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + decode_counter_bytes(N));
+  // partial slots first (fixed size), counters after: the counter region of one shape
+  // never overlaps another shape's partials in a shared workspace
+  float* partials = reinterpret_cast<float*>(ws);
+  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + decode_partials_bytes());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)P, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -820,19 +728,49 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16>, tw, tx, ts, tz, (uint16_t*)Y, counters,
+  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN>, tw, tx, ts, tz, (uint16_t*)Y, counters,
                             partials, M, N, wk, early);
+}
+
+// Fraction of the resident CTA slots kept busy by whole row blocks of height bn.
+double rowblock_utilization(int N, int bn, int slots) {
+  const int rbs = (N + bn - 1) / bn;
+  const int waves = (rbs + slots - 1) / slots;
+  return (double)rbs / ((double)waves * slots);
+}
+
+template <int MT, bool kBF16>
+cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                     void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
+  const int sched = option(SQ_OPT_DECODE_SCHEDULE);
+  const int slots = num_sms() * kMaxCtasPerSm;
+  const double u64 = rowblock_utilization(N, 64, slots), u32 = rowblock_utilization(N, 32, slots);
+  // AUTO: whole row blocks when they balance (>= 85 % of the slots busy) AND a stream-K
+  // CTA would stream so little (< 160 KB of codes) that its fixed cost -- the fixup round
+  // trips at the end of the kernel -- dominates; measured crossover on the 34B shapes
+  // (o_proj 8192 x 8192 takes row blocks, down_proj 8192 x 22016 stays stream-K).
+  const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
+      (double)((N + 63) / 64) * ((K / kGroup + GPS - 1) / GPS));
+  bool dp = false;
+  int bn = 64;
+  if (sched == SQ_SCHED_ROWBLOCK ||
+      (sched == SQ_SCHED_AUTO && std::max(u64, u32) >= 0.85 && sk_bytes_per_cta < 160.0 * 1024)) {
+    dp = true;
+    bn = u64 >= u32 ? 64 : 32;
+  }
+  if (bn == 32) return launch_t<MT, kBF16, 32>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
+  return launch_t<MT, kBF16, 64>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
 }
 
 }  // namespace
 
-size_t decode_counter_bytes(int64_t N) {
-  const int64_t RB = (N + BN - 1) / BN;
-  return (size_t)((RB * 4 + 255) / 256 * 256);
+size_t decode_partials_bytes() {
+  return (size_t)num_sms() * kMaxCtasPerSm * 2 * 16 * kMaxBN * sizeof(float);
 }
 
 size_t decode_workspace_bytes(int64_t N) {
-  return decode_counter_bytes(N) + (size_t)num_sms() * kMaxCtasPerSm * 2 * 16 * BN * sizeof(float);
+  const int64_t RB = (N + kMinBN - 1) / kMinBN;
+  return decode_partials_bytes() + (size_t)((RB * 4 + 255) / 256 * 256);
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
@@ -840,10 +778,10 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
                           cudaStream_t st, const char** why) {
   const bool bf16 = x_dtype == SQ_BF16;
   if (M <= 8)
-    return bf16 ? launch_t<1, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-                : launch_t<1, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
-  return bf16 ? launch_t<2, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-              : launch_t<2, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+    return bf16 ? launch_m<1, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+                : launch_m<1, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+  return bf16 ? launch_m<2, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+              : launch_m<2, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
 }
 
 }  // namespace sq

@@ -48,11 +48,13 @@ constexpr int kDecodeMaxM = 16;
 
 static int g_opt_pdl = 1;
 static int g_opt_weights_static = 0;
+static int g_opt_decode_schedule = SQ_SCHED_AUTO;
 
 int option(int opt) {
   switch (opt) {
     case SQ_OPT_PDL: return g_opt_pdl;
     case SQ_OPT_WEIGHTS_STATIC: return g_opt_weights_static;
+    case SQ_OPT_DECODE_SCHEDULE: return g_opt_decode_schedule;
     default: return -1;
   }
 }
@@ -86,6 +88,11 @@ sq_status sq_set_option(int opt, int value) {
   switch (opt) {
     case SQ_OPT_PDL: g_opt_pdl = value ? 1 : 0; return SQ_OK;
     case SQ_OPT_WEIGHTS_STATIC: g_opt_weights_static = value ? 1 : 0; return SQ_OK;
+    case SQ_OPT_DECODE_SCHEDULE:
+      if (value < SQ_SCHED_AUTO || value > SQ_SCHED_ROWBLOCK)
+        return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: decode schedule %d", value);
+      g_opt_decode_schedule = value;
+      return SQ_OK;
     default: return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: unknown option %d", opt);
   }
 }

@@ -19,7 +19,7 @@ cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t 
                             uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
                             cudaStream_t st);
 
-size_t decode_counter_bytes(int64_t N);
+size_t decode_partials_bytes();
 size_t decode_workspace_bytes(int64_t N);
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,

@@ -261,6 +261,31 @@ def test_gemm_chain_launch_options(pdl, static, M):
     assert _rel_frob(y, yr) <= 1e-2
 
 
+@pytest.mark.parametrize("sched", ["streamk", "rowblock"])
+def test_gemm_decode_schedules_shared_workspace(sched):
+    """Both decode schedules (SQ_OPT_DECODE_SCHEDULE) against the oracle, on one shared
+    default workspace: a small-N GEMM first, then shapes whose CTAs wrap the stage ring
+    after a row-block segment end (8192 x 8192: 7 stream-K units per CTA > 4 stages),
+    then the small one again; every result deterministic across launches."""
+    code = {"streamk": sq.SQ_SCHED_STREAMK, "rowblock": sq.SQ_SCHED_ROWBLOCK}[sched]
+    sq.set_option(sq.SQ_OPT_DECODE_SCHEDULE, code)
+    try:
+        for i, (N, K) in enumerate([(1024, 1024), (8192, 8192), (1536, 2048), (1024, 1024)]):
+            W = synth.weights(N, K, seed=90 + i)
+            ref = oracle.quantize_pack(W, None)
+            q = sq.quantize_pack_groupwise(_t(W))
+            for M in (1, 16):
+                X = synth.activations(M, K, seed=95 + i).astype(np.float16)
+                x = torch.from_numpy(X).to(DEV)
+                y_ref = oracle.gemm(X, ref["Wq"], ref["scales"], ref["zeros"], 128, "f16")
+                ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE) for _ in range(2)]
+                torch.cuda.synchronize()
+                assert _rel_frob(ys[0], y_ref) <= TIGHT[torch.float16], (N, K, M)
+                assert torch.equal(ys[0], ys[1]), (N, K, M)
+    finally:
+        sq.set_option(sq.SQ_OPT_DECODE_SCHEDULE, sq.SQ_SCHED_AUTO)
+
+
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("M", [1, 5, 16])
 def test_gemm_decode_streamk_fixup(M, dtype):

@@ -14,6 +14,8 @@ SHAPES = {"o": (8192, 8192), "gate": (8192, 22016), "gate_up": (8192, 44032), "d
 
 
 def bind(path):
+    """path[:opt=val,...] -- a library copy with its own process-wide options."""
+    path, _, opts = path.partition(":")
     L = ctypes.CDLL(path)
     vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
     L.sq_w4a16_gemm_path.argtypes = [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]
@@ -21,6 +23,9 @@ def bind(path):
     L.sq_w4a16_gemm_workspace_bytes.restype = sz
     L.sq_set_option.argtypes = [i32, i32]
     L.sq_set_option(2, 1)  # weights static
+    for kv in filter(None, opts.split(",")):
+        k, v = kv.split("=")
+        assert L.sq_set_option(int(k), int(v)) == 0
     return L
 
 
@@ -29,7 +34,7 @@ def main():
     path, ms = 1, (1, 16)
     if args and args[0] == "--prefill":
         path, ms, args = 2, (2048,), args[1:]
-    libs = [(os.path.basename(p), bind(p)) for p in args]
+    libs = [(os.path.basename(p), bind(p)) for p in args]  # name keeps any :opts suffix
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     launches = 48 if "--prefill" not in sys.argv else 8
