@@ -42,6 +42,9 @@ constexpr int kGroup = 128;
 #ifndef SQ_DEC_SX
 #define SQ_DEC_SX 0  // 1: magic-offset codes straight into the MMA + activation-sum correction
 #endif
+#ifndef SQ_DEC_SLEEP_NS
+#define SQ_DEC_SLEEP_NS 100000  // try_wait suspend-time hint of the producer / epilogue waits
+#endif
 #ifndef SQ_DEC_ABLATE
 #define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue
 #endif
@@ -101,6 +104,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
       "r"(parity)
+      : "memory");
+}
+// Same, for warps that wait long (producer, epilogue): the suspend-time hint lets the
+// hardware park the warp until the phase completes instead of re-polling, so the
+// wait loop does not take issue slots from the consumer warps on the same SMSP.
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(SQ_DEC_SLEEP_NS)
       : "memory");
 }
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
@@ -324,7 +341,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const uint32_t st = sbase + s * C::STAGE;
         const uint32_t fb = bar_full + 8 * s;
         if (i >= pre) {
-          mbar_wait(bar_empty + 8 * s, ph ^ 1);
+          mbar_wait_idle(bar_empty + 8 * s, ph ^ 1);
           mbar_expect_tx(fb, C::TX);
           load_weights(st, fb, sc.u);
         }
@@ -355,7 +372,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       if (sc.range_start(wk)) seg_begin_pos = pos;
       const bool rb_done = pos + 1 == wk.upb;
       if (rb_done || sc.range_last()) {
-        mbar_wait(red_full + 8 * s, (redph >> s) & 1u);
+        mbar_wait_idle(red_full + 8 * s, (redph >> s) & 1u);
         redph ^= 1u << s;
         const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODES);
         constexpr int W = C::XSLICE / 4;  // floats per warp slot

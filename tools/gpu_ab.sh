@@ -1,11 +1,4 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python bench.py > gpurun_out/bench_now.json 2> gpurun_out/bench_now.err; tail -3 gpurun_out/bench_now.err
-python -c "
-import json; d=json.loads(open('gpurun_out/bench_now.json').read().strip().splitlines()[-1])
-print('value', d['value'], d['unit'], 'frac', d['roofline']['frac'])
-for k,v in d.get('per_m',{}).items(): print(k, v)
-print('prefill', d.get('prefill'))
-print('e2e', d.get('e2e'))
-print('clocks', d.get('clocks'))
-"
+V=paper_2312_03788_b200/_lib/variants
+SQ_LIB=$PWD/$V/libsq_sleep.so timeout 600 python -m pytest tests -m gpu -x -q -k "decode or p13 or zero or auto or chain" 2>&1 | tail -2
+timeout 600 python tools/ab_decode.py $V/libsq_sk.so:3=1 $V/libsq_sleep.so:3=1 $V/libsq_rb.so:3=2 $V/libsq_sleep2.so:3=2 2>&1 | tail -8
