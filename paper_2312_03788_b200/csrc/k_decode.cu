@@ -733,7 +733,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // partial slots first (fixed size), counters after: the counter region of one shape
   // never overlaps another shape's partials in a shared workspace
   float* partials = reinterpret_cast<float*>(ws);
-  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + decode_partials_bytes());
+  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)P, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -787,7 +787,7 @@ size_t decode_partials_bytes() {
 
 size_t decode_workspace_bytes(int64_t N) {
   const int64_t RB = (N + kMinBN - 1) / kMinBN;
-  return decode_partials_bytes() + (size_t)((RB * 4 + 255) / 256 * 256);
+  return ws_partials_bytes() + (size_t)((RB * 4 + 255) / 256 * 256);
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,

@@ -50,7 +50,15 @@ constexpr int NSA = SQ_PRE_NSA;  // dequantized-A stages (TMEM, 32 columns each;
 constexpr int kDQW = SQ_PRE_DQW;
 constexpr int kDequantWarp0 = 4;
 constexpr int kThreads = (kDequantWarp0 + kDQW) * 32;
-constexpr int kColSplit = kDQW / 4;  // warps sharing a lane quarter split the k / token columns
+constexpr int kColSplit = kDQW / 4;  // warps sharing a lane quarter split the work / token columns
+#ifndef SQ_PRE_STAGESPLIT
+#define SQ_PRE_STAGESPLIT 1
+#endif
+// 8 dequant warps: the two warps of a lane quarter take alternate 64-k stages (k-halves of
+// each group) instead of the two 32-k halves of every stage, so two A stages are in flight
+// at once and the tcgen05.st -> wait::st -> arrive latency of one overlaps the other's math
+constexpr bool kStageSplit = SQ_PRE_STAGESPLIT && kColSplit == 2;
+constexpr int kAFullCount = kStageSplit ? kDQW / 2 : kDQW;
 
 constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
 constexpr int C_STAGE_BYTES = BM * (kGroup / 2);  // 8 KB
@@ -144,18 +152,25 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
+// The MMA issuer is a whole warp in warp-uniform control flow and the tcgen05 instruction is
+// predicated on elect.sync: the descriptors then live in uniform registers and one MMA
+// issues every few cycles.  Issued from a divergent single-lane branch instead, every MMA
+// pays a per-instruction uniform-register round trip (measured ~160-220 cycles per MMA,
+// tools/micro/mma_rate.cu, vs the 128-cycle tensor floor of a 128x256x16 MMA).
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   bar)
-               : "memory");
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                           uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
@@ -251,11 +266,55 @@ __device__ __forceinline__ void dequant8(uint32_t w, uint32_t zc, uint32_t d2, f
   }
 }
 
+// Work split of one CTA into segments (tile, groups [g0, g1)).  Tiles are (128-row
+// n-block, BT-token m-block), m fastest.  Without stream-K a CTA takes whole tiles c, c+P,
+// ...; with stream-K the (tile x group) units are split into equal contiguous ranges and a
+// tile cut between CTAs is finished by a fixup (last contributor sums the fp32 partials in
+// CTA order).
+struct PSched {
+  int c, P, G, tiles, sk, q, r;
+  int u, ue, tile, g0, g1;
+  bool first;
+  __device__ __forceinline__ int start(int cc) const { return cc * q + min(cc, r); }
+  __device__ __forceinline__ int cta_of(int v) const {
+    const int big = (q + 1) * r;
+    return v < big ? v / (q + 1) : r + (v - big) / q;
+  }
+  __device__ __forceinline__ PSched(int c_, int P_, int G_, int tiles_, int sk_, int q_, int r_)
+      : c(c_), P(P_), G(G_), tiles(tiles_), sk(sk_), q(q_), r(r_), first(true) {
+    if (sk) {
+      u = start(c);
+      ue = start(c + 1);
+      set();
+    } else {
+      tile = c;
+      g0 = 0;
+      g1 = G;
+    }
+  }
+  __device__ __forceinline__ void set() {
+    tile = u / G;
+    g0 = u % G;
+    g1 = min(G, g0 + (ue - u));
+  }
+  __device__ __forceinline__ bool valid() const { return sk ? u < ue : tile < tiles; }
+  __device__ __forceinline__ void next() {
+    first = false;
+    if (sk) {
+      u += g1 - g0;
+      set();
+    } else {
+      tile += P;
+    }
+  }
+};
+
 template <bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
-               uint16_t* __restrict__ Y, int M, int N, int K, int early_weights) {
+               uint16_t* __restrict__ Y, int M, int N, int K, int early_weights, int x_bytes,
+               int sk, int cta_q, int cta_r, float* __restrict__ partials, int* __restrict__ counters) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -281,7 +340,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
     for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), kDQW); }
-    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), kDQW); mbar_init(a_empty(i), 1); }
+    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), kAFullCount); mbar_init(a_empty(i), 1); }
     mbar_init(d_full, 1);
     mbar_init(d_empty, kDQW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -311,15 +370,16 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       pdl_wait();  // X may be the previous kernel's output
       int xs = 0;
       uint32_t xph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
+        const int tile = sc.tile;
         const int m0 = (tile % m_tiles) * BT;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 2 * sc.g0; kb < 2 * sc.g1; ++kb) {
           mbar_wait(x_empty(xs), xph ^ 1);
           PTS(5, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
           if (SQ_PRE_ABLATE & 1) {
             mbar_arrive(x_full(xs));
           } else {
-            mbar_expect_tx(x_full(xs), X_STAGE_BYTES);
+            mbar_expect_tx(x_full(xs), x_bytes);
             tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
           }
           if (++xs == NSX) { xs = 0; xph ^= 1; }
@@ -332,9 +392,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       if (!early_weights) pdl_wait();
       int cs = 0;
       uint32_t cph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
+        const int tile = sc.tile;
         const int n0 = (tile / m_tiles) * BM;
-        for (int g = 0; g < G; ++g) {
+        for (int g = sc.g0; g < sc.g1; ++g) {
           mbar_wait(c_empty(cs), cph ^ 1);
           PTS(4, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
           if (SQ_PRE_ABLATE & 2) {
@@ -350,22 +411,24 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
+    // ===================== MMA issuer: the whole warp, warp-uniform, elect.sync issues =====
+    {
       int xs = 0, as = 0;
       uint32_t xph = 0, aph = 0, dph = 0;
 #if SQ_PRE_TRACE
       unsigned long long tr[4] = {0, 0, 0, 0};
       const long long t_all = clock64();
 #endif
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
+        const int tile = sc.tile;
         const int m0 = (tile % m_tiles) * BT;
         const int n_mma = min(BT, ((M - m0) + 15) & ~15);
         const uint32_t idesc = make_idesc(kBF16, n_mma);
         PTW(0, mbar_wait(d_empty, dph ^ 1));  // epilogue has drained the accumulator
         dph ^= 1;
         tc_fence_after();
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = 2 * sc.g0;
+        for (int kb = kb0; kb < 2 * sc.g1; ++kb) {
           PTW(1, mbar_wait(a_full(as), aph));
           PTS(0, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
           PTW(2, mbar_wait(x_full(xs), xph));
@@ -376,7 +439,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint32_t a_tmem = tmem_base + A_COL + (uint32_t)as * (BK / 2) + (uint32_t)kk * 8;
             const uint64_t bdesc = make_sw128_desc(xaddr + kk * 32);
-            tc_mma_ts(tmem_base + D_COL, a_tmem, bdesc, idesc, (kb | kk) ? 1u : 0u);
+            tc_mma_ts(tmem_base + D_COL, a_tmem, bdesc, idesc, (kb != kb0 || kk) ? 1u : 0u);
           }
           tc_commit(x_empty(xs));
           tc_commit(a_empty(as));
@@ -398,15 +461,50 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int cs = 0, as = 0;
     uint32_t cph = 0, aph = 0, dph = 0;
+    int ai = 0;  // A-ring stage counter (stage-split mode)
 #if SQ_PRE_TRACE
     unsigned long long tr[4] = {0, 0, 0, 0};
     const long long t_all = clock64();
 #endif
     uint32_t abl_sink = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
+      const int tile = sc.tile;
       const int n0 = (tile / m_tiles) * BM;
       const int m0 = (tile % m_tiles) * BT;
-      for (int g = 0; g < G; ++g) {
+      for (int g = sc.g0; g < sc.g1; ++g) {
+        if constexpr (kStageSplit) {
+          mbar_wait(c_full(cs), cph);
+          const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
+          const int sw = (row >> 1) & 3;  // SWIZZLE_64B: chunk c sits at c ^ ((row >> 1) & 3)
+          const uint4 c0v = *reinterpret_cast<const uint4*>(crow + (((2 * ch) ^ sw) << 4));
+          const uint4 c1v = *reinterpret_cast<const uint4*>(crow + (((2 * ch + 1) ^ sw) << 4));
+          const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
+          const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(c_empty(cs));
+          if (++cs == NSC) { cs = 0; cph ^= 1; }
+          const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), __ushort_as_half(zbits)));
+          const __half2 d2h = __half2half2(__ushort_as_half(sbits));
+          const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
+          const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
+          const float df = __half2float(__ushort_as_half(sbits));
+          const uint32_t words[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
+          uint32_t a[32];
+#pragma unroll
+          for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+          // this warp's stage: k-half ch of the group -> A-ring index ai + ch
+          const int i = ai + ch;
+          const int slot = i % NSA;
+          mbar_wait(a_empty(slot), ((i / NSA) & 1) ^ 1);
+          tc_fence_after();
+          tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)slot * (BK / 2), a);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full(slot));
+          ai += 2;
+          continue;
+        }
         PTW(0, mbar_wait(c_full(cs), cph));
         if (lane == 0 && warp == kDequantWarp0) PTS(2, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
         const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
@@ -488,27 +586,69 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       tc_fence_after();
       const int n = n0 + row;
       const int mt = min(BT, M - m0);
+      auto to_out = [](float f) -> uint16_t {
+        return kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f)) : __half_as_ushort(__float2half_rn(f));
+      };
+      const bool full = sc.g0 == 0 && sc.g1 == G;
+      // stream-K partial tile: fp32 [token][row] slot of this CTA (0: first segment, 1: last)
+      float* slot = partials + ((size_t)blockIdx.x * 2 + (sc.first ? 0 : 1)) * (BT * BM);
       // warps sharing a lane quarter take alternating 16-token column blocks
       for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
         uint32_t v[16];
         tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
         tmem_ld_wait();
-        if (n < N) {
+        if (full) {
+          if (n < N) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int m = m0 + c0 + i;
-            if (c0 + i < mt) {
-              const float f = __uint_as_float(v[i]);
-              const uint16_t o = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
-                                       : __half_as_ushort(__float2half_rn(f));
-              Y[(size_t)m * N + n] = o;
-            }
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < mt) Y[(size_t)(m0 + c0 + i) * N + n] = to_out(__uint_as_float(v[i]));
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < mt) __stcg(slot + (c0 + i) * BM + row, __uint_as_float(v[i]));
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(d_empty);
+      if (lane == 0) mbar_arrive(d_empty);  // the accumulator is free for the next segment
+      if (!full) {
+        // fixup, overlapping the next segment's MMAs: the dequant warps' partial stores are
+        // published by one acq_rel atomic after a barrier among them
+        int* flag = reinterpret_cast<int*>(smem + OFF_TMEM + 8);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");
+        const int c_lo = sc.cta_of(tile * G), c_hi = sc.cta_of(tile * G + G - 1);
+        if (threadIdx.x == kDequantWarp0 * 32) {
+          int prev;
+          asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;\n"
+                       : "=r"(prev) : "l"(counters + tile) : "memory");
+          *flag = prev == c_hi - c_lo;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");
+        if (*flag) {
+          if (n < N) {
+            for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
+              float acc[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
+              for (int cc = c_lo; cc <= c_hi; ++cc) {
+                const int e = (sc.start(cc) / G == tile) ? 0 : 1;
+                const float* src = partials + ((size_t)cc * 2 + e) * (BT * BM) + row;
+                float pv[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pv[i] = (c0 + i < mt) ? __ldcg(src + (c0 + i) * BM) : 0.0f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc[i] += pv[i];
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < mt) Y[(size_t)(m0 + c0 + i) * N + n] = to_out(acc[i]);
+            }
+          }
+          if (threadIdx.x == kDequantWarp0 * 32) counters[tile] = 0;  // leave the workspace zeroed
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");  // flag reuse
+      }
 #if SQ_PRE_TRACE
       tr[3] += clock64() - t_ep;
 #endif
@@ -580,8 +720,8 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
 }
 __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
   asm volatile(
-      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n"
+      "{\n.reg .b16 m;\n.reg .pred e;\nmov.b16 m, 3;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n"
       ::"r"(bar)
       : "memory");
 }
@@ -589,9 +729,10 @@ __device__ __forceinline__ void tc_mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem,
                                                uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
@@ -695,8 +836,8 @@ prefill2_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer: one thread of the leader CTA =====================
-    if (leader && lane == 0) {
+    // ===================== MMA issuer: the leader CTA's warp (elect.sync issues) =====================
+    if (leader) {
       int xs = 0, as = 0;
       uint32_t xph = 0, aph = 0, dph = 0;
 #if SQ_PRE_TRACE
@@ -878,16 +1019,35 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 
 }  // namespace
 
-size_t prefill_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
+size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * BT * BM * sizeof(float); }
+
+// Stream-K over (tile x group) units when whole tiles would leave more than 5 % of the
+// last wave idle (mid-M shapes, and M = 2048 on the 8192-wide o/down/qkv layers).
+bool prefill_streamk(int64_t M, int64_t N, int64_t K) {
+  if (SQ_PRE_2CTA) return false;
+  const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int64_t P = num_sms();
+  const int64_t waves = (tiles + P - 1) / P;
+  return (double)tiles / (double)(waves * P) < 0.95 && tiles * (K / kGroup) >= P;
+}
+
+size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  if (!prefill_streamk(M, N, K)) return 0;
+  const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  return ws_partials_bytes() + (size_t)((tiles * 4 + 255) / 256 * 256);
+}
 
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K, void*, size_t,
+                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, size_t,
                            cudaStream_t st, const char** why) {
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = K / kGroup;
   const bool pair = SQ_PRE_2CTA != 0;
+  // X box: only as many token rows as the problem has (OOB rows would still cross the
+  // crossbar as zero fill)
+  const int x_rows = pair ? p2::BT2 / 2 : std::min(BT, (M + 15) / 16 * 16);
   bool ok = encode_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_UINT16, X, (uint64_t)K, (uint64_t)M,
-                      (uint64_t)K * 2, BK, pair ? p2::BT2 / 2 : BT, CU_TENSOR_MAP_SWIZZLE_128B);
+                      (uint64_t)K * 2, BK, x_rows, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
                        (uint64_t)K / 2, kGroup / 2, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G,
@@ -900,11 +1060,18 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
   }
   const int num_tiles = pair ? ((N + 2 * BM - 1) / (2 * BM)) * ((M + p2::BT2 - 1) / p2::BT2)
                             : ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
-  const int grid = pair ? 2 * std::min(num_tiles, num_sms() / 2) : std::min(num_tiles, num_sms());
-  auto kern = pair ? (x_dtype == SQ_BF16 ? prefill2_kernel<true> : prefill2_kernel<false>)
-                   : (x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>);
+  const bool sk = prefill_streamk(M, N, K);
+  const int units = num_tiles * G;
+  const int grid = pair ? 2 * std::min(num_tiles, num_sms() / 2)
+                        : (sk ? std::min(units, num_sms()) : std::min(num_tiles, num_sms()));
+  const int cta_q = units / grid, cta_r = units % grid;
+  float* partials = reinterpret_cast<float*>(ws);
+  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
+  auto kern1 = x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>;
+  auto kern2 = x_dtype == SQ_BF16 ? prefill2_kernel<true> : prefill2_kernel<false>;
   const int smem = pair ? p2::SMEM_ALLOC : SMEM_ALLOC;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = pair ? cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                       : cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid, 1, 1);
@@ -921,7 +1088,11 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
-  e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early);
+  if (pair)
+    e = cudaLaunchKernelEx(&cfg, kern2, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early);
+  else
+    e = cudaLaunchKernelEx(&cfg, kern1, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early,
+                           x_rows * BK * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -46,6 +46,8 @@ int num_sms() {
 
 constexpr int kDecodeMaxM = 16;
 
+size_t ws_partials_bytes() { return std::max(decode_partials_bytes(), prefill_partials_bytes()); }
+
 static int g_opt_pdl = 1;
 static int g_opt_weights_static = 0;
 static int g_opt_decode_schedule = SQ_SCHED_AUTO;
@@ -188,8 +190,8 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
   }
   if (path == SQ_PATH_PREFILL) {
     const size_t need = prefill_workspace_bytes(M, N, K);
-    if (need > 0 && (workspace == nullptr || workspace_bytes < need))
-      return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes", need);
+    if (need > 0 && (workspace == nullptr || workspace_bytes < need || !aligned16(workspace)))
+      return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
     cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K,
                                    workspace, workspace_bytes, st, &why);

@@ -19,7 +19,13 @@ cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t 
                             uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
                             cudaStream_t st);
 
+// GEMM workspace layout: [fp32 partial tiles: ws_partials_bytes()][int counters].  The
+// partial region has one fixed size for every shape and path, so no call's counters ever
+// overlap another call's partials in a shared workspace.
 size_t decode_partials_bytes();
+size_t prefill_partials_bytes();
+size_t ws_partials_bytes();
+bool prefill_streamk(int64_t M, int64_t N, int64_t K);
 size_t decode_workspace_bytes(int64_t N);
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,

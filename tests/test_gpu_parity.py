@@ -261,6 +261,24 @@ def test_gemm_chain_launch_options(pdl, static, M):
     assert _rel_frob(y, yr) <= 1e-2
 
 
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("M,N,K", [(64, 2048, 4096), (300, 1024, 4096), (520, 8192, 512), (17, 4096, 2048),
+                                   (128, 2816, 1024)])
+def test_gemm_prefill_streamk(M, N, K, dtype):
+    """Prefill shapes whose tiles leave the last wave mostly idle, so the (tile x group)
+    units are split between CTAs (stream-K) and finished by the fixup: ragged token
+    tiles, whole tiles in the middle of a CTA's range, several CTAs per tile.  Bit-identical
+    on every launch (fixed summation order)."""
+    y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M + N)
+    err = _rel_frob(y, y_ref)
+    assert err <= TOL_FROB and err <= TIGHT[dtype], err
+    x = torch.randn(M, K, device=DEV).to(dtype)
+    q = sq.quantize_pack_groupwise(torch.randn(N, K, device=DEV).half() * 0.02)
+    ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_PREFILL) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(ys[0], yy) for yy in ys[1:])
+
+
 @pytest.mark.parametrize("sched", ["streamk", "rowblock"])
 def test_gemm_decode_schedules_shared_workspace(sched):
     """Both decode schedules (SQ_OPT_DECODE_SCHEDULE) against the oracle, on one shared

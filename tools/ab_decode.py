@@ -34,14 +34,17 @@ def main():
     path, ms = 1, (1, 16)
     if args and args[0] == "--prefill":
         path, ms, args = 2, (2048,), args[1:]
+    if args and args[0].startswith("--ms="):
+        ms, args = tuple(int(v) for v in args[0][5:].split(",")), args[1:]
     libs = [(os.path.basename(p), bind(p)) for p in args]  # name keeps any :opts suffix
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    launches = 48 if "--prefill" not in sys.argv else 8
+    cold = path == 1 or min(ms) < 512  # rotate weight copies (> 4 x L2) when HBM-bound
+    launches = 48 if cold else 8
     res = {}
     for name, (K, N) in SHAPES.items():
         wb = K * N // 2 + 4 * N * K // 128
-        copies = max(2, (4 * l2) // wb + 1) if "--prefill" not in sys.argv else 2
+        copies = max(2, (4 * l2) // wb + 1) if cold else 2
         W = (torch.randn(N, K, device=dev) * 0.02).half()
         q0 = sq.quantize_pack_groupwise(W)
         del W
@@ -80,7 +83,7 @@ def main():
                     torch.cuda.synchronize()
                     times[lname].append(e0.elapsed_time(e1) * 1e3 / launches)
             B = wb + 2 * M * K + 2 * M * N
-            if path == 2:
+            if path == 2 and M >= 128:
                 B = 2 * M * N * K * 6532.2 / 1657.7  # report the fraction of the dense fp16 peak
             row = {"shape": name, "M": M}
             for ln, ts in times.items():

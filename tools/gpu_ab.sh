@@ -1,4 +1,6 @@
 set -x
 V=paper_2312_03788_b200/_lib/variants
-SQ_LIB=$PWD/$V/libsq_sleep.so timeout 600 python -m pytest tests -m gpu -x -q -k "decode or p13 or zero or auto or chain" 2>&1 | tail -2
-timeout 600 python tools/ab_decode.py $V/libsq_sk.so:3=1 $V/libsq_sleep.so:3=1 $V/libsq_rb.so:3=2 $V/libsq_sleep2.so:3=2 2>&1 | tail -8
+timeout 900 python -m pytest tests -m gpu -x -q -k "prefill or p13 or zero or auto" 2>&1 | tail -2
+SQ_LIB=$PWD/$V/libsq_pair.so timeout 900 python -m pytest tests -m gpu -x -q -k "prefill_parity or p13" 2>&1 | tail -2
+timeout 600 python tools/ab_decode.py --prefill $V/libsq_pbase.so $V/libsq_pcs.so $V/libsq_pel.so $V/libsq_pair.so 2>&1 | tail -4
+timeout 900 python tools/ab_decode.py --prefill --ms=17,64,128 $V/libsq_pcs.so $V/libsq_pel.so 2>&1 | tail -12

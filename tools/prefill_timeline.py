@@ -20,7 +20,7 @@ def main():
     q = sq.quantize_pack_groupwise((torch.randn(N, K, device="cuda") * 0.02).half())
     x = torch.randn(M, K, device="cuda").half()
     y = torch.empty(M, N, device="cuda", dtype=torch.half)
-    ws = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(1 << 20, sq.w4a16_gemm_workspace_bytes(M, N, K)), dtype=torch.uint8, device="cuda")
     for _ in range(3):
         st = L.sq_w4a16_gemm_path(x.data_ptr(), 0, q.Wq.data_ptr(), q.scales.data_ptr(), q.zeros.data_ptr(),
                                   y.data_ptr(), M, N, K, 128, ws.data_ptr(), ws.numel(), 2,
