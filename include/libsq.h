@@ -80,9 +80,15 @@ enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
  *    CTAs finished by a deterministic fixup through the workspace.
  *    SQ_SCHED_ROWBLOCK: whole row blocks (32 or 64 rows) per CTA, no fixup.
  *    AUTO takes ROWBLOCK when its wave quantization keeps >= 85 % of the CTAs
- *    busy, STREAMK otherwise.  Results agree to fp32 rounding either way. */
-enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2, SQ_OPT_DECODE_SCHEDULE = 3 };
+ *    busy, STREAMK otherwise.  Results agree to fp32 rounding either way.
+ *  SQ_OPT_DECODE_KERNEL (default SQ_DECK_MMA_SYNC): the decode-path kernel.
+ *    SQ_DECK_MMA_SYNC: warp-level mma.sync on register fragments (k_decode.cu).
+ *    SQ_DECK_TCGEN05: 5th-gen tensor cores, weights as the 128-row A operand in TMEM,
+ *    one TMEM accumulator per group (k_decode_tc.cu).  Same numerics (exact q - Z
+ *    operands, Δ applied per group in fp32). */
+enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2, SQ_OPT_DECODE_SCHEDULE = 3, SQ_OPT_DECODE_KERNEL = 4 };
 enum { SQ_SCHED_AUTO = 0, SQ_SCHED_STREAMK = 1, SQ_SCHED_ROWBLOCK = 2 };
+enum { SQ_DECK_MMA_SYNC = 0, SQ_DECK_TCGEN05 = 1 };
 
 /* Library version (major*10000 + minor*100 + patch). */
 SQ_API int sq_version(void);

@@ -1023,8 +1023,11 @@ size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * BT * BM * sizeo
 
 // Stream-K over (tile x group) units when whole tiles would leave more than 5 % of the
 // last wave idle (mid-M shapes, and M = 2048 on the 8192-wide o/down/qkv layers).
+#ifndef SQ_PRE_SK
+#define SQ_PRE_SK 1  // development: 0 = never split K between CTAs
+#endif
 bool prefill_streamk(int64_t M, int64_t N, int64_t K) {
-  if (SQ_PRE_2CTA) return false;
+  if (SQ_PRE_2CTA || !SQ_PRE_SK) return false;
   const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
   const int64_t P = num_sms();
   const int64_t waves = (tiles + P - 1) / P;

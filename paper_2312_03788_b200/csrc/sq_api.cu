@@ -46,17 +46,21 @@ int num_sms() {
 
 constexpr int kDecodeMaxM = 16;
 
-size_t ws_partials_bytes() { return std::max(decode_partials_bytes(), prefill_partials_bytes()); }
+size_t ws_partials_bytes() {
+  return std::max({decode_partials_bytes(), decode_tc_partials_bytes(), prefill_partials_bytes()});
+}
 
 static int g_opt_pdl = 1;
 static int g_opt_weights_static = 0;
 static int g_opt_decode_schedule = SQ_SCHED_AUTO;
+static int g_opt_decode_kernel = SQ_DECK_MMA_SYNC;
 
 int option(int opt) {
   switch (opt) {
     case SQ_OPT_PDL: return g_opt_pdl;
     case SQ_OPT_WEIGHTS_STATIC: return g_opt_weights_static;
     case SQ_OPT_DECODE_SCHEDULE: return g_opt_decode_schedule;
+    case SQ_OPT_DECODE_KERNEL: return g_opt_decode_kernel;
     default: return -1;
   }
 }
@@ -94,6 +98,11 @@ sq_status sq_set_option(int opt, int value) {
       if (value < SQ_SCHED_AUTO || value > SQ_SCHED_ROWBLOCK)
         return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: decode schedule %d", value);
       g_opt_decode_schedule = value;
+      return SQ_OK;
+    case SQ_OPT_DECODE_KERNEL:
+      if (value != SQ_DECK_MMA_SYNC && value != SQ_DECK_TCGEN05)
+        return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: decode kernel %d", value);
+      g_opt_decode_kernel = value;
       return SQ_OK;
     default: return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: unknown option %d", opt);
   }
@@ -184,7 +193,9 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
     if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: decode needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
-    cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why);
+    cudaError_t e = g_opt_decode_kernel == SQ_DECK_TCGEN05
+                        ? launch_decode_tc(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why)
+                        : launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
     return cuda_status(e, "decode");
   }

@@ -24,6 +24,10 @@ cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t 
 // overlap another call's partials in a shared workspace.
 size_t decode_partials_bytes();
 size_t prefill_partials_bytes();
+size_t decode_tc_partials_bytes();
+cudaError_t launch_decode_tc(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                             const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
+                             cudaStream_t st, const char** why);
 size_t ws_partials_bytes();
 bool prefill_streamk(int64_t M, int64_t N, int64_t K);
 size_t decode_workspace_bytes(int64_t N);

@@ -27,7 +27,8 @@ LIB_PATH = os.environ.get("SQ_LIB") or os.path.join(_HERE, "_lib", "libsq.so")
 SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
 SQ_F16, SQ_BF16 = 0, 1
 SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
-SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC, SQ_OPT_DECODE_SCHEDULE = 1, 2, 3
+SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC, SQ_OPT_DECODE_SCHEDULE, SQ_OPT_DECODE_KERNEL = 1, 2, 3, 4
+SQ_DECK_MMA_SYNC, SQ_DECK_TCGEN05 = 0, 1
 SQ_SCHED_AUTO, SQ_SCHED_STREAMK, SQ_SCHED_ROWBLOCK = 0, 1, 2
 GROUP = 128
 

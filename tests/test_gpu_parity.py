@@ -279,6 +279,28 @@ def test_gemm_prefill_streamk(M, N, K, dtype):
     assert all(torch.equal(ys[0], yy) for yy in ys[1:])
 
 
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("M", [1, 3, 8, 9, 16])
+@pytest.mark.parametrize("N,K", [(512, 512), (264, 1152), (2048, 4096), (8192, 8192)])
+def test_gemm_decode_tcgen05_parity(M, N, K, dtype):
+    """The tcgen05 decode kernel (SQ_OPT_DECODE_KERNEL = SQ_DECK_TCGEN05): ragged row
+    blocks (N = 264), ragged 4-group stages (K = 1152 = 9 groups), stream-K fixups and a
+    wrapping stage ring (8192 x 8192), against the oracle; deterministic."""
+    sq.set_option(sq.SQ_OPT_DECODE_KERNEL, sq.SQ_DECK_TCGEN05)
+    try:
+        y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_DECODE, seed=M + 7, smooth=N <= 2048)
+        err = _rel_frob(y, y_ref)
+        assert err <= TOL_FROB and err <= TIGHT[dtype], err
+        if N == 8192:
+            x = torch.randn(M, K, device=DEV).to(dtype)
+            q = sq.quantize_pack_groupwise(torch.randn(N, K, device=DEV).half() * 0.02)
+            ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE) for _ in range(3)]
+            torch.cuda.synchronize()
+            assert all(torch.equal(ys[0], yy) for yy in ys[1:])
+    finally:
+        sq.set_option(sq.SQ_OPT_DECODE_KERNEL, sq.SQ_DECK_MMA_SYNC)
+
+
 @pytest.mark.parametrize("sched", ["streamk", "rowblock"])
 def test_gemm_decode_schedules_shared_workspace(sched):
     """Both decode schedules (SQ_OPT_DECODE_SCHEDULE) against the oracle, on one shared
