@@ -245,11 +245,37 @@ struct Work {
   }
 };
 
-// Walks the units of one CTA in processing order (identical in all three warp roles).
+// Walks the units of one CTA in processing order (identical in all three warp roles) as
+// segments: contiguous unit ranges inside one row block.  Stream-K processes a CTA's
+// partial row blocks (the head and tail of its range) FIRST and its whole row blocks
+// after them, so the fixups of cut row blocks overlap the rest of the stream and the
+// kernel ends on plain Y stores instead of fixup round trips.
 struct Sched {
   int c, P, ri, nr, u, ue;
+  int u0, u1, hp, tp, nparts, f_lo;
+  bool full;  // the segment is a whole row block (direct Y store)
+  int e;      // partial-slot index: 0 = head of the CTA's range, 1 = tail
   __device__ __forceinline__ Sched(const Work& wk, int c_, int P_) : c(c_), P(P_), ri(0) {
-    nr = wk.dp ? (wk.rbs - c + P - 1) / P : 1;
+    if (wk.dp) {
+      nr = (wk.rbs - c + P - 1) / P;
+    } else {
+      u0 = wk.start(c);
+      u1 = wk.start(c + 1);
+      const int rb_a = u0 / wk.upb, rb_b = (u1 - 1) / wk.upb;
+      if (rb_a == rb_b) {
+        hp = 1;
+        tp = 0;
+        nparts = 1;
+        nr = 1;
+      } else {
+        hp = u0 % wk.upb != 0;
+        tp = u1 % wk.upb != 0;
+        nparts = hp + tp;
+        f_lo = hp ? rb_a + 1 : rb_a;
+        const int f_hi = tp ? rb_b - 1 : rb_b;
+        nr = nparts + max(0, f_hi - f_lo + 1);
+      }
+    }
     load(wk);
   }
   __device__ __forceinline__ void load(const Work& wk) {
@@ -257,15 +283,32 @@ struct Sched {
     if (wk.dp) {
       u = (c + ri * P) * wk.upb;
       ue = u + wk.upb;
+      full = true;
+      e = 0;
+    } else if (nr == 1 && nparts == 1 && hp && (u1 - 1) / wk.upb == u0 / wk.upb) {
+      u = u0;  // the whole range lies in one row block
+      ue = u1;
+      full = (u0 % wk.upb == 0) && (u1 - u0 == wk.upb);
+      e = 0;
+    } else if (ri < nparts) {
+      if (hp && ri == 0) {
+        u = u0;
+        ue = (u0 / wk.upb + 1) * wk.upb;
+        e = 0;
+      } else {
+        u = ((u1 - 1) / wk.upb) * wk.upb;
+        ue = u1;
+        e = 1;
+      }
+      full = false;
     } else {
-      u = wk.start(c);
-      ue = wk.start(c + 1);
+      u = (f_lo + ri - nparts) * wk.upb;
+      ue = u + wk.upb;
+      full = true;
+      e = 0;
     }
   }
   __device__ __forceinline__ bool valid() const { return ri < nr; }
-  __device__ __forceinline__ bool range_start(const Work& wk) const {
-    return wk.dp ? (u % wk.upb == 0) : (u == wk.start(c));
-  }
   __device__ __forceinline__ bool range_last() const { return u + 1 == ue; }
   __device__ __forceinline__ void next(const Work& wk) {
     if (++u == ue) {
@@ -365,13 +408,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     constexpr int E = C::MPAD * BN / 32;  // elements per lane
     int s = 0;
     uint32_t redph = 0;                   // phase bit per stage
-    int seg_begin_pos = 0;
-    bool first_seg = true, waited = false;
+    bool waited = false;
     for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
-      const int rb = sc.u / wk.upb, pos = sc.u % wk.upb;
-      if (sc.range_start(wk)) seg_begin_pos = pos;
-      const bool rb_done = pos + 1 == wk.upb;
-      if (rb_done || sc.range_last()) {
+      const int rb = sc.u / wk.upb;
+      if (sc.range_last()) {
         mbar_wait_idle(red_full + 8 * s, (redph >> s) & 1u);
         redph ^= 1u << s;
         const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODES);
@@ -392,7 +432,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const int n0 = rb * BN;
         if (SQ_DEC_ABLATE == 8) {
           if (v[0] == 1234.5f) Y[0] = 1;
-        } else if (seg_begin_pos == 0 && rb_done) {
+        } else if (sc.full) {
 #pragma unroll
           for (int i = 0; i < E; ++i) {
             const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
@@ -402,7 +442,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
           if (v[0] == 1234.5f) Y[0] = 1;
         } else {
           // stream-K fixup: park the partial; the last contributor sums them in CTA order
-          float* slot = partials + ((size_t)c * 2 + (first_seg ? 0 : 1)) * (16 * kMaxBN);
+          float* slot = partials + ((size_t)c * 2 + sc.e) * (16 * kMaxBN);
 #pragma unroll
           for (int i = 0; i < E; ++i) {
             const int idx = lane + 32 * i;
@@ -444,8 +484,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
             if (lane == 0) counters[rb] = 0;  // leave the workspace zeroed
           }
         }
-        first_seg = false;
-        seg_begin_pos = 0;
       }
       if (++s == C::NS) s = 0;
     }
@@ -616,7 +654,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
 
     // ---- end of a row-block segment?
-    const bool seg_end = (sc.u % wk.upb) + 1 == wk.upb || sc.range_last();
+    const bool seg_end = sc.range_last();
     __syncwarp();
     if (!seg_end) {
       if (lane == 0) mbar_arrive(bar_empty + 8 * s);
