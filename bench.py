@@ -397,7 +397,7 @@ def main():
         M = a.prefill_m
         pst = stack.LinearStack(model, rank, world, layers=st.layers[: a.prefill_layers], group=pg)
         pb = stack.make_buffers(pst, M, dev)
-        nbytes = sq.w4a16_gemm_workspace_bytes(M, 8192, 22016)
+        nbytes = max(sq.w4a16_gemm_workspace_bytes(M, sh.N, sh.K) for sh in pst.shards)
         ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
         for _ in range(2):
             stack.run_pass(pst, pb, workspace=ws)

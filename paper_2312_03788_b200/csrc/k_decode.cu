@@ -825,7 +825,7 @@ size_t decode_partials_bytes() {
 
 size_t decode_workspace_bytes(int64_t N) {
   const int64_t RB = (N + kMinBN - 1) / kMinBN;
-  return ws_partials_bytes() + (size_t)((RB * 4 + 255) / 256 * 256);
+  return ws_partials_bytes() + counter_region_bytes(RB);
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,

@@ -1021,8 +1021,10 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 
 size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * BT * BM * sizeof(float); }
 
-// Stream-K over (tile x group) units when whole tiles would leave more than 5 % of the
-// last wave idle (mid-M shapes, and M = 2048 on the 8192-wide o/down/qkv layers).
+// Stream-K over (tile x group) units when whole tiles would leave > 5 % of the last wave
+// idle at mid M (one token tile), or > 10 % on a long-K shape at large M (down_proj at
+// M = 2048).  Elsewhere the CTAs sweeping k in lockstep share X and W tiles in L2, which
+// stream-K's staggered ranges give up (measured: o_proj/qkv at M = 2048 are faster without).
 #ifndef SQ_PRE_SK
 #define SQ_PRE_SK 1  // development: 0 = never split K between CTAs
 #endif
@@ -1031,13 +1033,18 @@ bool prefill_streamk(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
   const int64_t P = num_sms();
   const int64_t waves = (tiles + P - 1) / P;
-  return (double)tiles / (double)(waves * P) < 0.95 && tiles * (K / kGroup) >= P;
+  const double eff = (double)tiles / (double)(waves * P);
+  if (tiles * (K / kGroup) < P) return false;
+#ifdef SQ_PRE_SK_ALWAYS
+  return eff < 0.95;
+#endif
+  return M <= BT ? eff < 0.95 : (eff < 0.9 && K >= 16384);
 }
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (!prefill_streamk(M, N, K)) return 0;
   const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
-  return ws_partials_bytes() + (size_t)((tiles * 4 + 255) / 256 * 256);
+  return ws_partials_bytes() + counter_region_bytes(tiles);
 }
 
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,

@@ -29,6 +29,12 @@ cudaError_t launch_decode_tc(const void* X, int x_dtype, const uint8_t* Wq, cons
                              const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
                              cudaStream_t st, const char** why);
 size_t ws_partials_bytes();
+// Counter region after the partials: at least 64 KB (16384 row blocks / tiles), so one
+// workspace sized for any of the usual shapes serves them all.
+inline size_t counter_region_bytes(int64_t counters) {
+  const size_t b = (size_t)((counters * 4 + 255) / 256 * 256);
+  return b < 65536 ? 65536 : b;
+}
 bool prefill_streamk(int64_t M, int64_t N, int64_t K);
 size_t decode_workspace_bytes(int64_t N);
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
