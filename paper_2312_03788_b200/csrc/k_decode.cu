@@ -15,8 +15,8 @@
 //    slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free).
 //  * Four consumer warps: warp w takes group w of every stage for all BN rows, so
 //    its X fragment is loaded (and k-permuted with PRMT) once and reused BN/16
-//    times.  Codes are turned into the EXACT integer (q - Z) in fp16/bf16 with the
-//    lop3 magic-number trick and fed to mma.sync.m16n8k16 with fp32 accumulation;
+//    times (SQ_DEC_CW = 8 splits the rows over two warps per group instead).  Codes
+//    are turned into the EXACT integer (q - Z) in fp16/bf16 with the lop3 magic-number trick and fed to mma.sync.m16n8k16 with fp32 accumulation;
 //    Δ is applied once per group to the accumulator fragment.
 //  * At the end of a row-block segment the consumer warps park their fp32 partial
 //    sums in SMEM (over their own, already consumed, activation slice of the stage)
@@ -48,8 +48,26 @@ constexpr int kGroup = 128;
 #ifndef SQ_DEC_ABLATE
 #define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue
 #endif
-constexpr int GPS = 4;          // groups per stage = consumer warps
-constexpr int kConsumerWarps = 4;
+#ifndef SQ_DEC_CW
+#define SQ_DEC_CW 4  // consumer warps: GPS groups x (SQ_DEC_CW / GPS) row slices of a stage
+                     // (8 = two warps per group: measured slower, kept as a tuning knob)
+#endif
+#ifndef SQ_DEC_TRACE
+#define SQ_DEC_TRACE 0  // development: per-CTA globaltimer trace (sq_debug_decode_trace)
+#endif
+#if SQ_DEC_TRACE
+__device__ long long* g_dec_trace = nullptr;  // [tickets][8]
+__device__ int g_dec_ticket = 0;
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
+#endif
+constexpr int GPS = 4;          // groups per stage
+constexpr int kConsumerWarps = SQ_DEC_CW;
+constexpr int kRowSplit = kConsumerWarps / GPS;  // warps sharing one group's rows
+static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multiple of GPS");
 constexpr int kProducerWarp = kConsumerWarps;      // TMA
 constexpr int kEpilogueWarp = kConsumerWarps + 1;  // cross-warp sum, output / stream-K fixup
 constexpr int kThreads = (kConsumerWarps + 2) * 32;
@@ -61,7 +79,8 @@ constexpr int kSmemBudget = 112 * 1024;  // per CTA, two CTAs per SM
 template <int MT, int BN>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
-  static constexpr int RT = BN / 16;                      // 16-row tiles per consumer warp
+  static constexpr int RT = BN / 16 / kRowSplit;          // 16-row tiles per consumer warp
+  static_assert(RT >= 1, "row block too short for the consumer split");
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
   static constexpr int XB = GPS * MPAD * kGroup * 2;      // 8 / 16 KB
   static constexpr int SZ = GPS * BN * 2;
@@ -349,6 +368,21 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+#if SQ_DEC_TRACE
+  __shared__ long long* tr_row;
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(&g_dec_ticket, 1);
+    tr_row = g_dec_trace ? g_dec_trace + (size_t)t * 8 : nullptr;
+    if (tr_row) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %smid;\n" : "=r"(smid));
+      tr_row[0] = gtime();
+      tr_row[4] = smid;
+      tr_row[5] = blockIdx.x;
+    }
+  }
+  __syncthreads();
+#endif
   // the next kernel in the stream may start its prologue as our CTAs retire
   pdl_launch_dependents();
 
@@ -377,6 +411,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
+#if SQ_DEC_TRACE
+      if (tr_row) tr_row[6] = gtime();
+#endif
       int s = 0;
       uint32_t ph = 0;
       int i = 0;
@@ -415,7 +452,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         mbar_wait_idle(red_full + 8 * s, (redph >> s) & 1u);
         redph ^= 1u << s;
         const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODES);
-        constexpr int W = C::XSLICE / 4;  // floats per warp slot
+        constexpr int W = C::XSLICE / 4;  // floats per group slot
         float v[E];
 #pragma unroll
         for (int i = 0; i < E; ++i) {
@@ -487,11 +524,15 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       }
       if (++s == C::NS) s = 0;
     }
+#if SQ_DEC_TRACE
+    if (lane == 0 && tr_row) tr_row[3] = gtime();
+#endif
     return;
   }
 
-  // ===================== consumers: warp w = group w of each stage =====================
+  // ===== consumers: warp w = group (w % GPS), rows [roff, roff + BN / kRowSplit) of each stage =====
   const int r = lane / 4, j = lane % 4;
+  const int grp = warp % GPS, roff = (warp / GPS) * (BN / kRowSplit);
   float acc[C::RT][MT][4];
 #pragma unroll
   for (int rt = 0; rt < C::RT; ++rt)
@@ -502,10 +543,16 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   int s = 0;
   uint32_t ph = 0;
+#if SQ_DEC_TRACE
+  bool first = true;
+#endif
   for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
     mbar_wait(bar_full + 8 * s, ph);
+#if SQ_DEC_TRACE
+    if (first && warp == 0 && lane == 0 && tr_row) tr_row[1] = gtime();
+    first = false;
+#endif
     const uint32_t st = sbase + s * C::STAGE;
-    const int grp = warp;
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
 #pragma unroll
@@ -546,8 +593,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       }
     }
     // codes of this warp's group: [group][row][64 B]
-    const uint32_t cbase = st + grp * (BN * 64) + r * 64 + j * 16;
-    const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
+    const uint32_t cbase = st + grp * (BN * 64) + (roff + r) * 64 + j * 16;
+    const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + (roff + r) * 2;
     const uint32_t sbz = sbs + C::SZ;
 #pragma unroll
     for (int rt = 0; rt < C::RT; ++rt) {
@@ -661,12 +708,16 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     } else {
       // park this warp's partial sums over its own activation slice of the stage and hand
       // them to the epilogue warp, which also releases the stage; no CTA-wide barrier
-      float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::CODES + warp * C::XSLICE);
+      // (the warps of one group write disjoint rows of the group's slot, after all of them
+      // have read their activation fragments from it: named barrier 1 + grp)
+      if (kRowSplit > 1)
+        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * kRowSplit) : "memory");
+      float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::CODES + grp * C::XSLICE);
 #pragma unroll
       for (int rt = 0; rt < C::RT; ++rt)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
+          const int t0 = 8 * mt + 2 * j, ra = roff + rt * 16 + r;
           slot[t0 * BN + ra] = acc[rt][mt][0];
           slot[(t0 + 1) * BN + ra] = acc[rt][mt][1];
           slot[t0 * BN + ra + 8] = acc[rt][mt][2];
@@ -682,6 +733,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
     if (++s == C::NS) { s = 0; ph ^= 1; }
   }
+#if SQ_DEC_TRACE
+  if (warp == 0 && lane == 0 && tr_row) tr_row[2] = gtime();
+#endif
 }
 
 // ------------------------------------------------------------------ host side
@@ -840,3 +894,14 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
 }
 
 }  // namespace sq
+
+#if SQ_DEC_TRACE
+// development only: per-CTA trace rows [start, first data, consumers done, epilogue done,
+// smid, blockIdx, -, -] in launch-ticket order (ticket counter reset by this call)
+extern "C" __attribute__((visibility("default"))) int sq_debug_decode_trace(void* dev_buf) {
+  long long* p = static_cast<long long*>(dev_buf);
+  int z = 0;
+  if (cudaMemcpyToSymbol(sq::g_dec_trace, &p, sizeof(p)) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(sq::g_dec_ticket, &z, sizeof(z)) != cudaSuccess;
+}
+#endif

@@ -36,13 +36,17 @@ def main():
         path, ms, args = 2, (2048,), args[1:]
     if args and args[0].startswith("--ms="):
         ms, args = tuple(int(v) for v in args[0][5:].split(",")), args[1:]
+    shapes = SHAPES
+    if args and args[0].startswith("--shapes="):  # K:N,K:N,...
+        shapes = {s: tuple(int(v) for v in s.split(":")) for s in args[0][9:].split(",")}
+        args = args[1:]
     libs = [(os.path.basename(p), bind(p)) for p in args]  # name keeps any :opts suffix
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     cold = path == 1 or min(ms) < 512  # rotate weight copies (> 4 x L2) when HBM-bound
     launches = 48 if cold else 8
     res = {}
-    for name, (K, N) in SHAPES.items():
+    for name, (K, N) in shapes.items():
         wb = K * N // 2 + 4 * N * K // 128
         copies = max(2, (4 * l2) // wb + 1) if cold else 2
         W = (torch.randn(N, K, device=dev) * 0.02).half()
