@@ -12,7 +12,9 @@
 //    chosen per shape by wave quantization.
 //  * One producer warp streams each unit with TMA into an SMEM ring: packed codes
 //    (3-D box 64 B x BN rows x 4 groups), the scale/zero rows and the matching X
-//    slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free).
+//    slice (4-D box, SWIZZLE_128B so the fragment reads are bank-conflict free).  At M = 1
+//    the box stages the one real token row (the MMA's other seven B columns are zeros
+//    supplied in registers), so a stage is 17.5 KB instead of 24.5 KB.
 //  * Four consumer warps: warp w takes group w of every stage for all BN rows, so
 //    its X fragment is loaded (and k-permuted with PRMT) once and reused BN/16
 //    times (SQ_DEC_CW = 8 splits the rows over two warps per group instead).  Codes
@@ -71,18 +73,23 @@ static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multi
 constexpr int kProducerWarp = kConsumerWarps;      // TMA
 constexpr int kEpilogueWarp = kConsumerWarps + 1;  // cross-warp sum, output / stream-K fixup
 constexpr int kThreads = (kConsumerWarps + 2) * 32;
-constexpr int kMaxCtasPerSm = SQ_DEC_CTAS;
+#ifndef SQ_DEC_CTAS_M1
+#define SQ_DEC_CTAS_M1 2  // CTAs per SM of the M = 1 kernel (1-token activation box; 3 measured slower)
+#endif
+constexpr int kMaxCtasPerSm = SQ_DEC_CTAS > SQ_DEC_CTAS_M1 ? SQ_DEC_CTAS : SQ_DEC_CTAS_M1;
 constexpr int kMaxBN = 64;      // row-block heights: 32 or 64
 constexpr int kMinBN = 32;
-constexpr int kSmemBudget = 112 * 1024;  // per CTA, two CTAs per SM
 
-template <int MT, int BN>
+// MT: 8-token MMA n-tiles; XR: token rows of the activation box actually staged (M = 1 stages
+// one row, the MMA sees zeros for the other seven); CT: resident CTAs per SM (smem budget)
+template <int MT, int BN, int XR, int CT>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
+  static constexpr int kSmemBudget = (CT <= 2 ? 112 : 74) * 1024;  // per CTA
   static constexpr int RT = BN / 16 / kRowSplit;          // 16-row tiles per consumer warp
   static_assert(RT >= 1, "row block too short for the consumer split");
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
-  static constexpr int XB = GPS * MPAD * kGroup * 2;      // 8 / 16 KB
+  static constexpr int XB = GPS * XR * kGroup * 2;        // 1 / 8 / 16 KB
   static constexpr int SZ = GPS * BN * 2;
   // stage bases stay 1024-B aligned (SWIZZLE_128B destination of the X box)
   static constexpr int TX = CODES + XB + 2 * SZ;  // bytes the TMA delivers per stage
@@ -91,7 +98,8 @@ struct Cfg {
   // At a segment end each consumer warp parks its fp32 partial sums (MPAD x BN) over its
   // own group's activation slice of the stage, which only that warp reads.
   static constexpr int XSLICE = XB / GPS;
-  static_assert(MPAD * BN * 4 <= XSLICE, "partial-sum slot must fit the activation slice");
+  static_assert(XR * BN * 4 <= XSLICE, "partial-sum slot must fit the activation slice");
+  static_assert(XR * BN >= 32, "epilogue lanes");
   static constexpr int OFF_BAR = NS * STAGE;  // full[NS], empty[NS], red_full[NS]
   static constexpr int SMEM = OFF_BAR + 3 * NS * 8;
   static constexpr int SMEM_ALLOC = SMEM + 1024;
@@ -342,13 +350,13 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-template <int MT, bool kBF16, int BN>
-__global__ void __launch_bounds__(kThreads, kMaxCtasPerSm)
+template <int MT, bool kBF16, int BN, int XR, int CT>
+__global__ void __launch_bounds__(kThreads, CT)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
               int M, int N, Work wk, int early_weights) {
-  using C = Cfg<MT, BN>;
+  using C = Cfg<MT, BN, XR, CT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -442,7 +450,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     // Walks the same schedule as the consumers.  At each segment end it sums the four
     // warps' parked partials (fixed warp order), hands the stage back to the producer,
     // then writes Y (whole row block) or runs the stream-K fixup (partial row block).
-    constexpr int E = C::MPAD * BN / 32;  // elements per lane
+    constexpr int E = XR * BN / 32;  // elements per lane
     int s = 0;
     uint32_t redph = 0;                   // phase bit per stage
     bool waited = false;
@@ -557,12 +565,14 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     uint32_t xb[MT][4][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
-      const int R = (grp * C::MPAD + r + 8 * mt) * 2 + (j >> 1);  // 128-byte row of the swizzled box
+      const int t = r + 8 * mt;
+      const int R = (grp * XR + t) * 2 + (j >> 1);  // 128-byte row of the swizzled box
       const uint32_t rowaddr = st + C::CODES + R * 128;
       uint32_t xv[16];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint4 v = lds128(rowaddr + ((((j & 1) * 4 + i) ^ (R & 7)) << 4));
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (XR >= C::MPAD || t < XR) v = lds128(rowaddr + ((((j & 1) * 4 + i) ^ (R & 7)) << 4));
         xv[4 * i] = v.x; xv[4 * i + 1] = v.y; xv[4 * i + 2] = v.z; xv[4 * i + 3] = v.w;
       }
 #pragma unroll
@@ -718,10 +728,14 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t0 = 8 * mt + 2 * j, ra = roff + rt * 16 + r;
-          slot[t0 * BN + ra] = acc[rt][mt][0];
-          slot[(t0 + 1) * BN + ra] = acc[rt][mt][1];
-          slot[t0 * BN + ra + 8] = acc[rt][mt][2];
-          slot[(t0 + 1) * BN + ra + 8] = acc[rt][mt][3];
+          if (XR >= C::MPAD || t0 < XR) {
+            slot[t0 * BN + ra] = acc[rt][mt][0];
+            slot[t0 * BN + ra + 8] = acc[rt][mt][2];
+          }
+          if (XR >= C::MPAD || t0 + 1 < XR) {
+            slot[(t0 + 1) * BN + ra] = acc[rt][mt][1];
+            slot[(t0 + 1) * BN + ra + 8] = acc[rt][mt][3];
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
         }
@@ -764,25 +778,25 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MT, bool kBF16, int BN>
+template <int MT, bool kBF16, int BN, int XR, int CT>
 int ctas_per_sm() {
   static int cached = -1;
   if (cached < 0) {
     int n = 0;
-    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<MT, BN>::SMEM_ALLOC);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN>, kThreads,
-                                                      Cfg<MT, BN>::SMEM_ALLOC) != cudaSuccess || n < 1)
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT>, kThreads,
+                                                      Cfg<MT, BN, XR, CT>::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
-    cached = std::min(n, kMaxCtasPerSm);
+    cached = std::min(n, CT);
   }
   return cached;
 }
 
-template <int MT, bool kBF16, int BN>
+template <int MT, bool kBF16, int BN, int XR, int CT>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, bool dp, cudaStream_t st, const char** why) {
-  using C = Cfg<MT, BN>;
+  using C = Cfg<MT, BN, XR, CT>;
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
   {
@@ -797,7 +811,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   {
     const uint64_t d[4] = {64, 2, (uint64_t)M, (uint64_t)G};
     const uint64_t s[3] = {128, (uint64_t)K * 2, 256};
-    const uint32_t b[4] = {64, 2, (uint32_t)C::MPAD, GPS};
+    const uint32_t b[4] = {64, 2, (uint32_t)XR, GPS};
     if (!encode(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, X, d, s, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
       *why = "tensor map (X)";
       return cudaErrorInvalidValue;
@@ -818,7 +832,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   wk.upb = (G + GPS - 1) / GPS;
   wk.units = wk.rbs * wk.upb;
   wk.dp = dp ? 1 : 0;
-  const int slots = num_sms() * ctas_per_sm<MT, kBF16, BN>();
+  const int slots = num_sms() * ctas_per_sm<MT, kBF16, BN, XR, CT>();
   const int P = dp ? std::min(wk.rbs, slots) : std::min(wk.units, slots);
   wk.cta_q = wk.units / P;
   wk.cta_r = wk.units % P;
@@ -837,7 +851,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN>, tw, tx, ts, tz, (uint16_t*)Y, counters,
+  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT>, tw, tx, ts, tz, (uint16_t*)Y, counters,
                             partials, M, N, wk, early);
 }
 
@@ -848,11 +862,11 @@ double rowblock_utilization(int N, int bn, int slots) {
   return (double)rbs / ((double)waves * slots);
 }
 
-template <int MT, bool kBF16>
+template <int MT, bool kBF16, int XR, int CT>
 cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
-  const int slots = num_sms() * kMaxCtasPerSm;
+  const int slots = num_sms() * CT;
   const double u64 = rowblock_utilization(N, 64, slots), u32 = rowblock_utilization(N, 32, slots);
   // AUTO: whole row blocks when they balance (>= 85 % of the slots busy) AND a stream-K
   // CTA would stream so little (< 160 KB of codes) that its fixed cost -- the fixup round
@@ -867,8 +881,8 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     dp = true;
     bn = u64 >= u32 ? 64 : 32;
   }
-  if (bn == 32) return launch_t<MT, kBF16, 32>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
-  return launch_t<MT, kBF16, 64>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
+  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
+  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
 }
 
 }  // namespace
@@ -886,11 +900,15 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
                           cudaStream_t st, const char** why) {
   const bool bf16 = x_dtype == SQ_BF16;
+  constexpr int C2 = SQ_DEC_CTAS, C1 = SQ_DEC_CTAS_M1;
+  if (M == 1)  // batch-1 decode: stage one activation row, smaller stages, more CTAs per SM
+    return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+                : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
   if (M <= 8)
-    return bf16 ? launch_m<1, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-                : launch_m<1, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
-  return bf16 ? launch_m<2, true>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-              : launch_m<2, false>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+    return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+                : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+  return bf16 ? launch_m<2, true, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
+              : launch_m<2, false, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
 }
 
 }  // namespace sq
