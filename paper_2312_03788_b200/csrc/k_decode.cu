@@ -48,7 +48,8 @@ constexpr int kGroup = 128;
 #define SQ_DEC_SLEEP_NS 100000  // try_wait suspend-time hint of the producer / epilogue waits
 #endif
 #ifndef SQ_DEC_ABLATE
-#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue
+#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue,
+                         // 32 = no per-stage compute (pipeline skeleton)
 #endif
 #ifndef SQ_DEC_CW
 #define SQ_DEC_CW 4  // consumer warps: GPS groups x (SQ_DEC_CW / GPS) row slices of a stage
@@ -561,6 +562,12 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     first = false;
 #endif
     const uint32_t st = sbase + s * C::STAGE;
+    if (SQ_DEC_ABLATE == 32) {  // experiment: no per-stage compute at all (pipeline skeleton)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sc.range_last() ? red_full + 8 * s : bar_empty + 8 * s);
+      if (++s == C::NS) { s = 0; ph ^= 1; }
+      continue;
+    }
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
 #pragma unroll

@@ -44,11 +44,13 @@ def main():
     dev = "cuda"
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     cold = path == 1 or min(ms) < 512  # rotate weight copies (> 4 x L2) when HBM-bound
-    launches = 48 if cold else 8
+    if os.environ.get("AB_WARM_L2"):  # consumer-bound probe: one weight copy, L2-resident
+        cold = False
+    launches = 48 if cold or os.environ.get("AB_WARM_L2") else 8
     res = {}
     for name, (K, N) in shapes.items():
         wb = K * N // 2 + 4 * N * K // 128
-        copies = max(2, (4 * l2) // wb + 1) if cold else 2
+        copies = max(2, (4 * l2) // wb + 1) if cold else (1 if os.environ.get("AB_WARM_L2") else 2)
         W = (torch.randn(N, K, device=dev) * 0.02).half()
         q0 = sq.quantize_pack_groupwise(W)
         del W
