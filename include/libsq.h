@@ -184,6 +184,36 @@ SQ_API sq_status sq_w4a16_gemm_path(const void* X, int x_dtype,
                              void* Y, int64_t M, int64_t N, int64_t K, int group,
                              void* workspace, size_t workspace_bytes, int path, void* stream);
 
+/*
+ * ---- Calibration: single-layer smoothing-strength search ----
+ * The grid search over alpha in {0, 0.05, ..., 1} that minimizes
+ * the Eq. 4 loss  E(alpha) = || X W^T - Xhat_alpha What_alpha^T ||^2  of one layer
+ * is host logic (paper_2312_03788_b200/calib.py) over the calls above
+ * plus these two device steps.
+ */
+
+/*
+ * Activation side of Eq. 5: Xs[m][k] = RN_dtype(X[m][k] / s[k]),
+ * the quotient correctly rounded in fp64 and rounded once to x_dtype (bit-identical to
+ * the oracle's RN(fp64(X) / fp64(s))).  X, Xs: device [M][K] in x_dtype (may alias:
+ * in-place is allowed); s: device fp32[K] (> 0, e.g. from sq_smooth_scales).
+ * K % 8 == 0 and 16-byte aligned X/Xs (else SQ_ERR_ALIGN).  M == 0 is a no-op that
+ * returns SQ_OK without looking at the pointers (argument order: shape, dtype, null, align).
+ */
+SQ_API sq_status sq_smooth_activations(const void* X, int x_dtype, const float* s,
+                                int64_t M, int64_t K, void* Xs, void* stream);
+
+/*
+ * Squared Frobenius distance of Eq. 4: *out = sum_i (A[i] - B[i])^2 over n elements of
+ * two device arrays in `dtype` (fp16/bf16), accumulated in fp64 with a fixed reduction
+ * order (bit-reproducible run to run).  out: device double, written.  workspace: device,
+ * at least sq_sq_diff_sum_workspace_bytes() bytes (per-CTA partials), caller-owned.
+ * n == 0 writes 0 (A and B may then be null).
+ */
+SQ_API size_t sq_sq_diff_sum_workspace_bytes(void);
+SQ_API sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n,
+                         double* out, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

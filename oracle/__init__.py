@@ -18,6 +18,9 @@ degenerate groups, ...) are listed in DESIGN.md §3 and SURVEY.md §8(c) S1-S17.
 Pinning status (see DESIGN.md §3 and tests/test_oracle_pins.py):
   weight_absmax, act_absmax, smooth_scales, fold, quantize_group,
   quantize_pack, pack/unpack, dequant, gemm  -- pinned.
+  smooth_activations, alpha_grid, layer_loss,
+  alpha_search (N2)                          -- pinned (exact-rational X̂, zero-loss
+                                               layer + tie rule, permutation invariance).
   gemm summation order                      -- parity unpinned beyond tolerance
                                                (any order is a correct result).
 """
@@ -38,6 +41,10 @@ from .sq_oracle import (  # noqa: F401
     dequant,
     gemm,
     quant_loss,
+    smooth_activations,
+    alpha_grid,
+    layer_loss,
+    alpha_search,
     footprint_ratio,
     NONFINITE_SCALE_BITS,
 )

@@ -321,6 +321,61 @@ def quant_loss(X: np.ndarray, W: np.ndarray, W_hat: np.ndarray) -> float:
     return float((D * D).sum())
 
 
+# --------------------------------------------------------------------------
+# N2: single-layer smoothing-strength grid search
+# --------------------------------------------------------------------------
+
+def smooth_activations(X: np.ndarray, s: np.ndarray, x_dtype: str = "f16") -> np.ndarray:
+    """Activation side of Eq. 5: X̂ = X·diag(s)^-1, per input
+    channel k, as stored activations: RN(fp64(X) / fp64(s)) to x_dtype (fp16 array,
+    or uint16 bf16 bits).  fp64 division is correctly rounded, then rounded once."""
+    q = _as_f64(X, x_dtype) / np.asarray(s, dtype=np.float32).astype(np.float64)[None, :]
+    if x_dtype == "f16":
+        with np.errstate(over="ignore"):
+            return q.astype(np.float16)
+    if x_dtype == "bf16":
+        return rn_bf16_bits(q)
+    raise ValueError(x_dtype)
+
+
+def alpha_grid() -> np.ndarray:
+    """The smoothing strengths searched: 0 to 1 at an interval of 0.05 (PAPER.md:164
+    "grid search with an interval of 0.05 between 0 and 1"), 21 values,
+    each the double nearest to i/20."""
+    return np.array([i / 20.0 for i in range(21)], dtype=np.float64)
+
+
+def layer_loss(X: np.ndarray, W: np.ndarray, alpha: float, group: int = 128,
+               x_dtype: str = "f16", act_max=None) -> float:
+    """Eq. 4 of one smoothed, quantized layer:
+        E(α) = || X·W - X̂_α·Ŵ_α ||²,  X̂_α = RN(X/s_α) (Eq. 5 activation side),
+        Ŵ_α = dequant(Q(RN(W·s_α))) (Eq. 5 weight side + Eq. 1), s_α from Eq. 6
+    with act_max taken over the same X unless given.  Everything after the two stored
+    roundings (X̂, the codes/Δ/Z) is exact fp64."""
+    x = _as_f64(X, x_dtype)
+    if act_max is None:
+        act_max = act_absmax(X, x_dtype)
+    s = smooth_scales(weight_absmax(W), act_max, alpha)
+    q = quantize_pack(W, s, group)
+    x_hat = _as_f64(smooth_activations(X, s, x_dtype), x_dtype)
+    D = x @ _as_f64(W, "f16").T - x_hat @ dequant(q["Wq"], q["scales"], q["zeros"], group).T
+    return float((D * D).sum())
+
+
+def alpha_search(X: np.ndarray, W: np.ndarray, group: int = 128, x_dtype: str = "f16",
+                 alphas=None):
+    """Grid search of the smoothing strength for ONE layer: the α of
+    the grid with the smallest Eq. 4 loss; ties go to the smallest α (the first minimum
+    in grid order).  The paper minimizes the loss of the entire model (PAPER.md:164);
+    the per-layer objective is this repo's reading.
+    Returns (best_alpha, losses fp64[len(alphas)])."""
+    alphas = alpha_grid() if alphas is None else np.asarray(alphas, dtype=np.float64)
+    am = act_absmax(X, x_dtype)
+    losses = np.array([layer_loss(X, W, float(a), group, x_dtype, am) for a in alphas])
+    best = int(np.argmin(losses))  # numpy argmin returns the first minimum
+    return float(alphas[best]), losses
+
+
 def footprint_ratio(N: int, K: int, group: int = 128) -> float:
     """Bytes of the W4 layout (codes + fp16 Δ + fp16 Z per group) over fp16 bytes
     (PAPER.md:74 "reducing the memory footprint by approximately 75%")."""

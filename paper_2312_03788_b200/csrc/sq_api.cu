@@ -219,4 +219,33 @@ sq_status sq_w4a16_gemm(const void* X, int x_dtype, const uint8_t* Wq, const uin
                             workspace_bytes, SQ_PATH_AUTO, stream);
 }
 
+sq_status sq_smooth_activations(const void* X, int x_dtype, const float* s, int64_t M, int64_t K,
+                                void* Xs, void* stream) {
+  g_last_error.clear();
+  if (M < 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_smooth_activations: M=%lld K=%lld", (long long)M, (long long)K);
+  if (!valid_dtype(x_dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_activations: dtype %d", x_dtype);
+  if (M == 0) return SQ_OK;  // no-op (an empty X may have a null data pointer)
+  if (!X || !s || !Xs) return fail(SQ_ERR_NULL, "sq_smooth_activations: null pointer");
+  if (K % 8 != 0 || !aligned16(X) || !aligned16(Xs))
+    return fail(SQ_ERR_ALIGN, "sq_smooth_activations: K %% 8 != 0 or unaligned pointer");
+  return cuda_status(launch_smooth_activations(X, x_dtype, s, M, K, Xs, static_cast<cudaStream_t>(stream)),
+                     "sq_smooth_activations");
+}
+
+size_t sq_sq_diff_sum_workspace_bytes(void) { return (size_t)sq_diff_ctas() * sizeof(double); }
+
+sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, double* out, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  g_last_error.clear();
+  if ((n > 0 && (!A || !B)) || !out || !workspace) return fail(SQ_ERR_NULL, "sq_sq_diff_sum: null pointer");
+  if (n < 0) return fail(SQ_ERR_SHAPE, "sq_sq_diff_sum: n=%lld", (long long)n);
+  if (!valid_dtype(dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_sq_diff_sum: dtype %d", dtype);
+  if (workspace_bytes < sq_sq_diff_sum_workspace_bytes())
+    return fail(SQ_ERR_WORKSPACE, "sq_sq_diff_sum: workspace %zu < %zu", workspace_bytes,
+                sq_sq_diff_sum_workspace_bytes());
+  return cuda_status(launch_sq_diff_sum(A, B, dtype, n, static_cast<double*>(workspace), out,
+                                        static_cast<cudaStream_t>(stream)),
+                     "sq_sq_diff_sum");
+}
+
 }  // extern "C"

@@ -49,6 +49,13 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
 int num_sms();
 int option(int opt);
 
+// calibration (k_calib.cu)
+int sq_diff_ctas();
+cudaError_t launch_smooth_activations(const void* X, int dtype, const float* s, int64_t M, int64_t K,
+                                      void* Xs, cudaStream_t st);
+cudaError_t launch_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, double* partials,
+                               double* out, cudaStream_t st);
+
 // ---- small device helpers ----
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t and_mask, uint32_t or_mask) {
   uint32_t r;

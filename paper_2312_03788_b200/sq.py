@@ -63,6 +63,9 @@ def _load():
         "sq_w4a16_gemm_workspace_bytes": (sz, [i64, i64, i64, i32]),
         "sq_w4a16_gemm": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp]),
         "sq_w4a16_gemm_path": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]),
+        "sq_smooth_activations": (i32, [vp, i32, vp, i64, i64, vp, vp]),
+        "sq_sq_diff_sum_workspace_bytes": (sz, []),
+        "sq_sq_diff_sum": (i32, [vp, vp, i32, i64, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -76,7 +79,8 @@ EXPORTED = (
     "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_set_option",
     "sq_get_option", "sq_act_absmax",
     "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
-    "sq_w4a16_gemm", "sq_w4a16_gemm_path",
+    "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
+    "sq_sq_diff_sum",
 )
 
 
@@ -220,4 +224,33 @@ def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = N
     _check(_load().sq_w4a16_gemm_path(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
                                       _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes, int(path),
                                       _stream(stream)))
+    return out
+
+
+def smooth_activations(X: torch.Tensor, s: torch.Tensor, out: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor:
+    """X̂ = RN(X / s) per input channel (activation side of Eq. 5); out may be X (in place)."""
+    _need_cuda(X, s)
+    M, K = X.shape
+    if out is None:
+        out = torch.empty_like(X)
+    _check(_load().sq_smooth_activations(_ptr(X), _dtype_code(X), _ptr(s), M, K, _ptr(out), _stream(stream)))
+    return out
+
+
+def sq_diff_sum(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
+                workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Σ (A - B)² in fp64 (the squared norm of Eq. 4), deterministic; returns a device
+    float64 scalar tensor (no host sync)."""
+    _need_cuda(A, B)
+    if A.shape != B.shape or A.dtype != B.dtype:
+        raise ValueError("sq_diff_sum: A and B need the same shape and dtype")
+    L = _load()
+    nb = L.sq_sq_diff_sum_workspace_bytes()
+    if workspace is None:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=A.device)
+    if out is None:
+        out = torch.empty((), dtype=torch.float64, device=A.device)
+    _check(L.sq_sq_diff_sum(_ptr(A), _ptr(B), _dtype_code(A), A.numel(), _ptr(out), _ptr(workspace),
+                            workspace.numel() * workspace.element_size(), _stream(stream)))
     return out

@@ -103,3 +103,22 @@ def test_workspace_query(L):
 
 def test_decode_requires_workspace(L):
     assert _gemm(L, M=4, path=1) == sq.SQ_ERR_WORKSPACE
+
+
+def test_calib_argument_errors(L):
+    """N2 calibration calls reject bad arguments on the host (include/libsq.h)."""
+    f = L.sq_smooth_activations
+    assert f(None, 0, FAKE, 4, 128, FAKE, None) == sq.SQ_ERR_NULL
+    assert f(None, 0, None, 0, 128, None, None) == sq.SQ_OK  # empty: pointers unused
+    assert f(FAKE, 0, FAKE, -1, 128, FAKE, None) == sq.SQ_ERR_SHAPE
+    assert f(FAKE, 0, FAKE, 4, 0, FAKE, None) == sq.SQ_ERR_SHAPE
+    assert f(FAKE, 7, FAKE, 4, 128, FAKE, None) == sq.SQ_ERR_UNSUPPORTED
+    assert f(FAKE, 0, FAKE, 4, 124, FAKE, None) == sq.SQ_ERR_ALIGN
+    assert f(FAKE, 0, FAKE, 0, 128, FAKE, None) == sq.SQ_OK  # M == 0: no-op, no launch
+    nb = L.sq_sq_diff_sum_workspace_bytes()
+    assert nb >= 8
+    d = L.sq_sq_diff_sum
+    assert d(None, FAKE, 0, 10, FAKE, FAKE, nb, None) == sq.SQ_ERR_NULL
+    assert d(FAKE, FAKE, 0, -1, FAKE, FAKE, nb, None) == sq.SQ_ERR_SHAPE
+    assert d(FAKE, FAKE, 3, 10, FAKE, FAKE, nb, None) == sq.SQ_ERR_UNSUPPORTED
+    assert d(FAKE, FAKE, 0, 10, FAKE, FAKE, nb - 8, None) == sq.SQ_ERR_WORKSPACE

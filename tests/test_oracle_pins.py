@@ -369,3 +369,92 @@ def test_p14_tp_shards():
         p = oracle.quantize_pack(W[:, k0:k1], s[k0:k1], 128)
         parts = parts + oracle.gemm(X[:, k0:k1], p["Wq"], p["scales"], p["zeros"])
     assert np.allclose(parts, Y, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- N2: α grid search
+def test_n2_alpha_grid():
+    """PAPER.md:164 / :213: grid over [0, 1] at an interval of 0.05 -> 21 points."""
+    g = oracle.alpha_grid()
+    assert len(g) == 21 and g[0] == 0.0 and g[-1] == 1.0
+    assert np.allclose(np.diff(g), 0.05, atol=1e-15, rtol=0)
+    assert [Fraction(x).limit_denominator(20) for x in g] == [Fraction(i, 20) for i in range(21)]
+
+
+def test_n2_smooth_activations_exact_rational():
+    """X̂ = X·diag(s)^-1 (Eq. 5), stored once-rounded: the oracle's
+    fp64 route equals the exact-rational RN16 of x / s (third implementation), including
+    power-of-two s (exact scaling), s = 1 (identity) and random fp32 s."""
+    r = np.random.default_rng(11)
+    x = r.standard_normal((6, 64)).astype(np.float16)
+    x[0, :8] = np.array([0.0, -0.0, 65504.0, -65504.0, 6e-8, -6e-8, 1.0, 2049.0], dtype=np.float16)
+    for s in (np.full(64, 1.0, np.float32), np.full(64, 0.25, np.float32),
+              r.uniform(1e-3, 1e3, 64).astype(np.float32), r.uniform(0.9, 1.1, 64).astype(np.float32)):
+        got = oracle.smooth_activations(x, s)
+        for (i, k), xv in np.ndenumerate(x):
+            want = ex.rn_f16(Fraction(float(xv)) / Fraction(float(s[k])))
+            g = float(got[i, k])
+            if want is None:
+                assert np.isinf(g)
+            else:
+                assert Fraction(g) == want, (i, k, float(xv), float(s[k]))
+    assert np.array_equal(oracle.smooth_activations(x, np.ones(64, np.float32)).view(np.uint16), x.view(np.uint16))
+
+
+def _exact_layer(N=16, K=256, T=8, seed=3):
+    """A layer the pipeline reproduces exactly: every column max |W_k| = 1 and max |X_k| = 1
+    (so s = 1 for every α by Eq. 6), every group on the grid (q - 8)·0.125 with both q = 0
+    and q = 15 present (so Δ = 0.125, Z = 8 and Ŵ = W by Eq. 1)."""
+    r = np.random.default_rng(seed)
+    q = r.integers(0, 16, size=(N, K))
+    q[0, 0::2], q[0, 1::2] = 0, 15
+    q[1, 0::2], q[1, 1::2] = 15, 0
+    W = ((q - 8) * 0.125).astype(np.float16)
+    X = r.uniform(-1, 1, size=(T, K))
+    X[0, :] = 1.0
+    return X.astype(np.float16), W
+
+
+def test_n2_zero_loss_layer_and_tie_rule():
+    """Eq. 4 special case: when smoothing is the identity (s = 1) and W lies on the Eq. 1
+    grid, X̂ = X and Ŵ = W exactly, so E(α) = 0 for every α; all 21 tie and the search
+    returns the smallest α (the tie rule).  X = 0 likewise gives E = 0 everywhere."""
+    X, W = _exact_layer()
+    best, losses = oracle.alpha_search(X, W)
+    assert best == 0.0 and np.all(losses == 0.0)
+    best0, losses0 = oracle.alpha_search(np.zeros_like(X), W)
+    assert best0 == 0.0 and np.all(losses0 == 0.0)
+
+
+def test_n2_loss_invariant_under_channel_permutations():
+    """Eq. 4-6 are per input channel and per output channel: permuting whole groups of
+    input channels (X and W columns together) or output channels (W rows) permutes s
+    and the quantization groups but leaves every E(α) unchanged.  A fold or smoothing
+    along the wrong axis breaks this (N == K here)."""
+    X = synth.activations(32, 384, seed=5).astype(np.float16)
+    W = synth.weights(384, 384, seed=6)
+    a = [0.0, 0.35, 0.5, 1.0]
+    _, base = oracle.alpha_search(X, W, alphas=a)
+    pg = np.array([2, 0, 1])
+    cols = np.concatenate([np.arange(g * 128, (g + 1) * 128) for g in pg])
+    _, pk = oracle.alpha_search(X[:, cols], W[:, cols], alphas=a)
+    rows = np.random.default_rng(0).permutation(384)
+    _, pn = oracle.alpha_search(X, W[rows], alphas=a)
+    np.testing.assert_allclose(pk, base, rtol=1e-12)
+    np.testing.assert_allclose(pn, base, rtol=1e-12)
+    assert not np.allclose(base[0], base[2])  # α matters on this data
+
+
+def test_n2_search_under_outliers():
+    """×100 outlier channels amplify the weight quantization error; the
+    search picks an interior α whose loss is below both endpoints and below RTN (s = 1,
+    PAPER.md:206), and it is the argmin of the grid."""
+    X = synth.activations(64, 512, seed=7).astype(np.float16)
+    W = synth.weights(256, 512, seed=8)
+    best, losses = oracle.alpha_search(X, W)
+    assert 0.0 < best < 1.0
+    assert losses[int(round(best * 20))] == losses.min()
+    assert losses.min() < losses[0] and losses.min() < losses[-1]
+    q = oracle.quantize_pack(W, None)
+    x = X.astype(np.float64)
+    rtn = float(((x @ W.astype(np.float64).T - x @ oracle.dequant(q["Wq"], q["scales"], q["zeros"]).T) ** 2).sum())
+    assert losses.min() < rtn
