@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--prefill-layers", type=int, default=4)
     ap.add_argument("--skip-prefill", action="store_true")
     ap.add_argument("--skip-quant", action="store_true")
+    ap.add_argument("--skip-calib", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
@@ -461,6 +462,36 @@ def main():
                  "what": "sq_smooth_scales (w_max + Eq. 6) + sq_quantize_pack_groupwise for one layer"}
         del Ws
 
+    # ---------------- N2: single-layer α grid search (calibration)
+    calib_res = None
+    if not a.skip_calib and rank == 0:
+        from paper_2312_03788_b200 import calib
+
+        sh = max(st.shards, key=lambda x: x.N * x.K)  # the largest linear (34B gate|up)
+        T_cal = 164 * 128  # 164 HumanEval prompts x 128 tokens
+        Wc = stack.synth_weight(sh.N, sh.K, 4242, dev)
+        gen = torch.Generator(device=dev).manual_seed(4343)
+        Xc = torch.randn(T_cal, sh.K, device=dev, generator=gen)
+        oc = torch.randperm(sh.K, device=dev, generator=gen)[:8]
+        Xc[:, oc] *= 100.0  # fixed outlier channels
+        Xc = Xc.half()
+        calib.alpha_search(Xc, Wc, alphas=(0.0, 0.5))  # warm-up (allocations, first launches)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        best_a, losses = calib.alpha_search(Xc, Wc)
+        e1.record()
+        torch.cuda.synchronize()
+        t_c = e0.elapsed_time(e1) * 1e-3
+        calib_res = {"value": t_c, "unit": "s", "best_alpha": best_a,
+                     "loss_at_best_over_alpha0": float(losses.min() / losses[0]),
+                     "what": f"21-point α grid search (Eq. 4 loss) of one {sh.N}x{sh.K} linear, "
+                             f"T={T_cal} calibration tokens with 8 x100 outlier channels: per α "
+                             "smooth_scales + quantize + smooth_activations + W4A16 GEMM + fp64 loss; "
+                             "reference X·Wᵀ once by torch.matmul"}
+        del Wc, Xc
+        torch.cuda.empty_cache()
+
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.skip_cpu:
@@ -490,6 +521,7 @@ def main():
             "per_m": per_m,
             "prefill": prefill,
             "quantize": quant,
+            "calibration": calib_res,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
