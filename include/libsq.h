@@ -214,6 +214,48 @@ SQ_API size_t sq_sq_diff_sum_workspace_bytes(void);
 SQ_API sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n,
                          double* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * ---- Row-parallel all-reduce over peer memory ----
+ * After a row-parallel linear (o_proj, down_proj) every rank holds a partial Y[M][N]; the
+ * layer output is their sum (BASELINE.json north_star: "an all-reduce over NVLink after
+ * row-parallel layers").  Instead of a separate NCCL call this is a one-shot exchange in
+ * ONE kernel over NVLink/NVSwitch peer memory: each CTA pushes its chunk of the local
+ * partial into every rank's symmetric buffer, raises a per-chunk flag there, waits for
+ * the same chunk from every rank and sums the world partials in rank order (fp32, so all
+ * ranks get bit-identical Y).  Launched with PDL, so its prologue overlaps the GEMM tail.
+ *
+ * Symmetric buffer: each rank allocates sq_allreduce_buffer_bytes(n_max, world) bytes of
+ * device memory, ZERO-FILLED once, and shares it with its peers (sq_ipc_* below, or any
+ * peer mapping); peer_bufs is a DEVICE array of `world` device pointers, entry q = rank q's
+ * buffer as mapped in this process (entry `rank` = its own).  epoch: 0 = device-managed
+ * (the kernel takes the rank's buffer counter + 1 and advances it when done: safe under
+ * CUDA graph replay, since every rank makes the same sequence of calls); or an explicit
+ * 1, 2, 3, ... per call, the same on every rank (after 2^32 - 1 continue at 2).  Use one
+ * mode per buffer.
+ * n <= n_max elements of dtype (fp16/bf16) in y_local and y_out (may alias).  error_flag:
+ * device int, set to 1 if a peer did not arrive within the bounded wait (~seconds); the
+ * kernel then leaves y_out partially written instead of hanging.  Stream-ordered; every
+ * rank must make the matching call (a collective).
+ */
+SQ_API size_t sq_allreduce_buffer_bytes(int64_t n_max, int world);
+SQ_API sq_status sq_allreduce_oneshot(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,
+                               void* const* peer_bufs, int rank, int world, uint32_t epoch,
+                               int* error_flag, void* stream);
+
+/*
+ * CUDA IPC plumbing for the symmetric buffers (host calls, no stream work).
+ * sq_ipc_get_handle: export the cudaMalloc block containing dev_ptr into handle_out
+ * (sq_ipc_handle_bytes() bytes) and report dev_ptr's byte offset inside that block (a
+ * caching allocator may sub-allocate); the importer adds the offset to the mapped base.
+ * sq_ipc_open_handle: map a peer's handle in this process (enables peer access lazily)
+ * and return the block base; sq_ipc_close: unmap it.  A handle cannot be opened by the
+ * process that exported it.  The symmetric buffer needs n_max % 8 == 0 (16-B slots).
+ */
+SQ_API size_t sq_ipc_handle_bytes(void);
+SQ_API sq_status sq_ipc_get_handle(void* dev_ptr, void* handle_out, size_t* offset_out);
+SQ_API sq_status sq_ipc_open_handle(const void* handle, void** dev_ptr_out);
+SQ_API sq_status sq_ipc_close(void* dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

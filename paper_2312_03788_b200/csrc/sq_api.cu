@@ -6,6 +6,8 @@
 #include <cstring>
 #include <string>
 
+#include <cuda.h>
+
 #include "sq_internal.cuh"
 
 namespace sq {
@@ -246,6 +248,73 @@ sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, dou
   return cuda_status(launch_sq_diff_sum(A, B, dtype, n, static_cast<double*>(workspace), out,
                                         static_cast<cudaStream_t>(stream)),
                      "sq_sq_diff_sum");
+}
+
+size_t sq_allreduce_buffer_bytes(int64_t n_max, int world) {
+  if (n_max <= 0 || world <= 0) return 0;
+  return ar_buffer_bytes(n_max, world);
+}
+
+sq_status sq_allreduce_oneshot(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,
+                               void* const* peer_bufs, int rank, int world, uint32_t epoch, int* error_flag,
+                               void* stream) {
+  g_last_error.clear();
+  if (n < 0 || n_max < 0 || n > n_max || world <= 0 || rank < 0 || rank >= world)
+    return fail(SQ_ERR_SHAPE, "sq_allreduce_oneshot: n=%lld n_max=%lld rank=%d world=%d", (long long)n,
+                (long long)n_max, rank, world);
+  if (!valid_dtype(dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_allreduce_oneshot: dtype %d", dtype);
+  if ((n_max + ar_chunk_elems() - 1) / ar_chunk_elems() > kArMaxChunks)
+    return fail(SQ_ERR_UNSUPPORTED, "sq_allreduce_oneshot: n_max %lld > %lld", (long long)n_max,
+                (long long)kArMaxChunks * ar_chunk_elems());
+  if (n == 0) return SQ_OK;
+  if (!y_local || !y_out || !peer_bufs || !error_flag) return fail(SQ_ERR_NULL, "sq_allreduce_oneshot: null pointer");
+  if (!aligned16(y_local) || !aligned16(y_out) || !aligned16(peer_bufs) || n_max % 8 != 0)
+    return fail(SQ_ERR_ALIGN, "sq_allreduce_oneshot: unaligned pointer or n_max %% 8 != 0");
+  return cuda_status(launch_oneshot_allreduce(y_local, dtype, y_out, n, n_max, peer_bufs, rank, world, epoch,
+                                              error_flag, static_cast<cudaStream_t>(stream)),
+                     "sq_allreduce_oneshot");
+}
+
+size_t sq_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+sq_status sq_ipc_get_handle(void* dev_ptr, void* handle_out, size_t* offset_out) {
+  g_last_error.clear();
+  if (!dev_ptr || !handle_out || !offset_out) return fail(SQ_ERR_NULL, "sq_ipc_get_handle: null pointer");
+  // the handle names the whole cudaMalloc block; report where dev_ptr sits inside it
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(SQ_ERR_CUDA, "sq_ipc_get_handle: cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(SQ_ERR_CUDA, "sq_ipc_get_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_status(e, "sq_ipc_get_handle");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (size_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return SQ_OK;
+}
+
+sq_status sq_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  g_last_error.clear();
+  if (!handle || !dev_ptr_out) return fail(SQ_ERR_NULL, "sq_ipc_open_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess), "sq_ipc_open_handle");
+}
+
+sq_status sq_ipc_close(void* dev_ptr) {
+  g_last_error.clear();
+  if (!dev_ptr) return fail(SQ_ERR_NULL, "sq_ipc_close: null pointer");
+  return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "sq_ipc_close");
 }
 
 }  // extern "C"

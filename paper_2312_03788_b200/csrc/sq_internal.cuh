@@ -49,6 +49,14 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
 int num_sms();
 int option(int opt);
 
+// one-shot all-reduce over peer memory (k_allreduce.cu)
+constexpr int kArMaxChunks = 8192;  // 2048 outputs per chunk: n <= 16 Mi outputs per call
+int64_t ar_chunk_elems();
+size_t ar_buffer_bytes(int64_t n_max, int world);
+cudaError_t launch_oneshot_allreduce(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,
+                                     void* const* peers_dev, int rank, int world, uint32_t epoch, int* err,
+                                     cudaStream_t st);
+
 // calibration (k_calib.cu)
 int sq_diff_ctas();
 cudaError_t launch_smooth_activations(const void* X, int dtype, const float* s, int64_t M, int64_t K,

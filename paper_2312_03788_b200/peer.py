@@ -1,0 +1,60 @@
+"""Symmetric peer buffers and the one-shot row-parallel all-reduce.
+
+Plumbing only: torch allocates each rank's buffer and torch.distributed exchanges the
+CUDA IPC handles (libsq's sq_ipc_*); the exchange of the partial outputs is one kernel,
+sq_allreduce_oneshot (csrc/k_allreduce.cu), over NVLink/NVSwitch peer memory.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import sq
+
+
+class PeerAllReduce:
+    """Row-parallel all-reduce of up to n_max fp16/bf16 outputs per call, one instance per
+    process group.  Collective construction (every rank of `group` must build it)."""
+
+    def __init__(self, n_max: int, device, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n_max = (int(n_max) + 7) // 8 * 8
+        nb = sq.allreduce_buffer_bytes(self.n_max, self.world)
+        self.buf = torch.zeros(nb, dtype=torch.uint8, device=device)  # flags must start at 0
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        handle, off = sq.ipc_get_handle(self.buf)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, (handle, off), group=group)
+        self._opened = []
+        addrs = []
+        for q, (h, o) in enumerate(allh):
+            if q == self.rank:
+                addrs.append(self.buf.data_ptr())
+            else:
+                base = sq.ipc_open_handle(h)
+                self._opened.append(base)
+                addrs.append(base + o)
+        self.peers = torch.tensor(addrs, dtype=torch.int64, device=device)
+        dist.barrier(group=group)
+
+    def __call__(self, y: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """In place by default: y (this rank's partial) becomes the sum over ranks.  The epoch
+        is device-managed (epoch 0), so the call may be captured in a CUDA graph."""
+        if y.numel() > self.n_max:
+            raise ValueError(f"PeerAllReduce: {y.numel()} outputs > n_max {self.n_max}")
+        return sq.allreduce_oneshot(y, self.peers, self.rank, self.world, 0, self.n_max, self.err,
+                                    out=out, stream=stream)
+
+    def failed(self) -> bool:
+        """True if any call timed out waiting for a peer (host sync)."""
+        return bool(self.err.item())
+
+    def close(self):
+        torch.cuda.synchronize()
+        for base in self._opened:
+            sq.ipc_close(base)
+        self._opened = []

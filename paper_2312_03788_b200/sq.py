@@ -66,6 +66,12 @@ def _load():
         "sq_smooth_activations": (i32, [vp, i32, vp, i64, i64, vp, vp]),
         "sq_sq_diff_sum_workspace_bytes": (sz, []),
         "sq_sq_diff_sum": (i32, [vp, vp, i32, i64, vp, vp, sz, vp]),
+        "sq_allreduce_buffer_bytes": (sz, [i64, i32]),
+        "sq_allreduce_oneshot": (i32, [vp, i32, vp, i64, i64, vp, i32, i32, c.c_uint32, vp, vp]),
+        "sq_ipc_handle_bytes": (sz, []),
+        "sq_ipc_get_handle": (i32, [vp, vp, c.POINTER(sz)]),
+        "sq_ipc_open_handle": (i32, [vp, c.POINTER(vp)]),
+        "sq_ipc_close": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -80,7 +86,8 @@ EXPORTED = (
     "sq_get_option", "sq_act_absmax",
     "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
     "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
-    "sq_sq_diff_sum",
+    "sq_sq_diff_sum", "sq_allreduce_buffer_bytes", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
+    "sq_ipc_get_handle", "sq_ipc_open_handle", "sq_ipc_close",
 )
 
 
@@ -254,3 +261,42 @@ def sq_diff_sum(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = Non
     _check(L.sq_sq_diff_sum(_ptr(A), _ptr(B), _dtype_code(A), A.numel(), _ptr(out), _ptr(workspace),
                             workspace.numel() * workspace.element_size(), _stream(stream)))
     return out
+
+
+def allreduce_buffer_bytes(n_max: int, world: int) -> int:
+    return int(_load().sq_allreduce_buffer_bytes(int(n_max), int(world)))
+
+
+def allreduce_oneshot(y_local: torch.Tensor, peers_dev: torch.Tensor, rank: int, world: int, epoch: int,
+                      n_max: int, error_flag: torch.Tensor, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """One-shot all-reduce of the row-parallel partial y_local over peer memory
+    (include/libsq.h sq_allreduce_oneshot).  peers_dev: int64 device tensor of the world
+    symmetric-buffer addresses as mapped in this process."""
+    _need_cuda(y_local, peers_dev, error_flag)
+    if out is None:
+        out = y_local
+    _check(_load().sq_allreduce_oneshot(_ptr(y_local), _dtype_code(y_local), _ptr(out), y_local.numel(),
+                                        int(n_max), _ptr(peers_dev), int(rank), int(world),
+                                        ctypes.c_uint32(epoch & 0xFFFFFFFF), _ptr(error_flag), _stream(stream)))
+    return out
+
+
+def ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(handle bytes, byte offset of t inside its cudaMalloc block)."""
+    L = _load()
+    buf = ctypes.create_string_buffer(L.sq_ipc_handle_bytes())
+    off = ctypes.c_size_t(0)
+    _check(L.sq_ipc_get_handle(_ptr(t), buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open_handle(handle: bytes) -> int:
+    """Map a peer's block; returns its base device address in this process."""
+    p = ctypes.c_void_p()
+    _check(_load().sq_ipc_open_handle(ctypes.create_string_buffer(handle, len(handle)), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(addr: int) -> None:
+    _check(_load().sq_ipc_close(ctypes.c_void_p(addr)))

@@ -122,3 +122,28 @@ def test_calib_argument_errors(L):
     assert d(FAKE, FAKE, 0, -1, FAKE, FAKE, nb, None) == sq.SQ_ERR_SHAPE
     assert d(FAKE, FAKE, 3, 10, FAKE, FAKE, nb, None) == sq.SQ_ERR_UNSUPPORTED
     assert d(FAKE, FAKE, 0, 10, FAKE, FAKE, nb - 8, None) == sq.SQ_ERR_WORKSPACE
+
+
+def test_allreduce_argument_errors(L):
+    """One-shot all-reduce / IPC calls reject bad arguments on the host (include/libsq.h)."""
+    f = L.sq_allreduce_oneshot
+    ok = dict(n=1024, n_max=1024, rank=0, world=2, epoch=1)
+
+    def call(**kw):
+        a = {**ok, **kw}
+        return f(FAKE, kw.get("dtype", 0), FAKE, a["n"], a["n_max"], FAKE, a["rank"], a["world"], a["epoch"],
+                 kw.get("err", FAKE), None)
+
+    assert call(n=2048) == sq.SQ_ERR_SHAPE          # n > n_max
+    assert call(rank=2) == sq.SQ_ERR_SHAPE
+    assert call(world=0) == sq.SQ_ERR_SHAPE
+    assert call(dtype=5) == sq.SQ_ERR_UNSUPPORTED
+    assert call(n_max=1 << 40, n=8) == sq.SQ_ERR_UNSUPPORTED
+    assert call(err=None) == sq.SQ_ERR_NULL
+    assert call(n_max=1028, n=1028) == sq.SQ_ERR_ALIGN
+    assert call(n=0) == sq.SQ_OK
+    assert L.sq_allreduce_buffer_bytes(1024, 2) >= 2 * 2 * 1024 * 2
+    assert L.sq_ipc_handle_bytes() == 64
+    assert L.sq_ipc_get_handle(None, FAKE, None) == sq.SQ_ERR_NULL
+    assert L.sq_ipc_open_handle(None, None) == sq.SQ_ERR_NULL
+    assert L.sq_ipc_close(None) == sq.SQ_ERR_NULL

@@ -1,0 +1,160 @@
+"""One-shot row-parallel all-reduce over peer memory on one
+GPU.  The expected value is fixed by the definition, not by the kernel: every rank gets
+RN( ((0 + p_0) + p_1) + ... ) in fp32, rank order -- bit-exact, identical on all ranks.
+
+  * single process, one stream per "rank": the kernel's protocol (push, per-chunk flags,
+    wait, ordered reduce, epoch parity double buffering) with world 2 and 3, ragged sizes
+    and back-to-back calls;
+  * two processes (gloo for the handle exchange), CUDA IPC mapping of the symmetric
+    buffers (PeerAllReduce), several epochs, and the row-parallel layer of the TP stack
+    reduced with it against the unsharded oracle.
+The NVLink transport itself is not exercised (one GPU); the peer mapping and protocol are.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2312_03788_b200 import sq
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _expected(parts):
+    acc = torch.zeros_like(parts[0], dtype=torch.float32)
+    for p in parts:
+        acc = acc + p.float()
+    return acc.to(parts[0].dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("n", [8, 2048, 8192 * 16 + 5, 8192 * 64])
+@pytest.mark.parametrize("mode", ["explicit", "device"])
+def test_oneshot_protocol_streams(world, n, dtype, mode):
+    n_max = (n + 7) // 8 * 8 + 64
+    nb = sq.allreduce_buffer_bytes(n_max, world)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    errs = [torch.zeros(1, dtype=torch.int32, device=DEV) for _ in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    g = torch.Generator(device=DEV).manual_seed(n + world)
+    torch.cuda.synchronize()
+    for epoch in range(1, 6):  # back-to-back calls: both parities, reuse
+        parts = [torch.randn(n, generator=g, device=DEV).to(dtype) for _ in range(world)]
+        outs = [torch.empty_like(parts[0]) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                sq.allreduce_oneshot(parts[r], peers, r, world, epoch if mode == "explicit" else 0, n_max,
+                                     errs[r], out=outs[r], stream=streams[r])
+        torch.cuda.synchronize()
+        assert all(int(e.item()) == 0 for e in errs)
+        want = _expected(parts)
+        for r in range(world):
+            assert torch.equal(outs[r].view(torch.int16), want.view(torch.int16)), (epoch, r)
+
+
+def test_oneshot_in_place_and_timeout():
+    world, n = 2, 4096
+    n_max = n
+    nb = sq.allreduce_buffer_bytes(n_max, world)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    # rank 1 never arrives: the bounded wait must give up and flag it, not hang
+    y = torch.randn(n, device=DEV).half()
+    sq.allreduce_oneshot(y, peers, 0, world, 7, n_max, err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        import oracle
+        from paper_2312_03788_b200 import peer, synth, tp
+
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        ar = peer.PeerAllReduce(1 << 20, DEV)
+        ok = []
+        g = torch.Generator(device="cpu").manual_seed(1)
+        for it in range(4):
+            parts = [torch.randn(5000 + 8 * it, generator=g).half() for _ in range(world)]
+            y = parts[rank].to(DEV)
+            ar(y)
+            torch.cuda.synchronize()
+            ok.append(torch.equal(y.cpu().view(torch.int16), _expected(parts).view(torch.int16)))
+        # captured in a CUDA graph: the device-managed epoch advances on every replay
+        yg = torch.zeros(4096, dtype=torch.float16, device=DEV)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            ar(yg)  # warm-up on a side stream before capture
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ar(yg)
+        for it in range(3):
+            parts = [torch.randn(4096, generator=g).half() for _ in range(world)]
+            yg.copy_(parts[rank].to(DEV))
+            torch.cuda.synchronize()
+            dist.barrier()
+            graph.replay()
+            torch.cuda.synchronize()
+            ok.append(torch.equal(yg.cpu().view(torch.int16), _expected(parts).view(torch.int16)))
+        # row-parallel layer of the TP stack reduced through the peer buffers
+        model = tp.ModelShape("tiny-34b-like", hidden=1024, mlp=2816, layers=1, q_heads=8, kv_heads=2,
+                              head_dim=128)
+        for i, (name, K, N) in enumerate(tp.full_shapes(model)):
+            sh = tp.layer_shards(model, rank, world)[i]
+            if sh.kind != "row":
+                continue
+            W = synth.weights(N, K, seed=20 + i)
+            X = synth.activations(4, K, seed=30 + i).astype(np.float16)
+            k0, k1 = sh.k_range
+            qsh = sq.quantize_pack_groupwise(torch.from_numpy(np.ascontiguousarray(W[:, k0:k1])).to(DEV))
+            y = sq.w4a16_gemm(torch.from_numpy(np.ascontiguousarray(X[:, k0:k1])).to(DEV), qsh)
+            ar(y)
+            full = oracle.quantize_pack(W, None)
+            y_ref = oracle.gemm(X, full["Wq"], full["scales"], full["zeros"])
+            err = np.linalg.norm(y.float().cpu().double().numpy() - y_ref) / np.linalg.norm(y_ref)
+            ok.append(bool(err <= 2e-3))
+        ok.append(not ar.failed())
+        ar.close()
+        q.put((rank, all(ok)))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_peer_allreduce_two_processes_ipc():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
