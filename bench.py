@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--skip-prefill", action="store_true")
     ap.add_argument("--skip-quant", action="store_true")
     ap.add_argument("--skip-calib", action="store_true")
+    ap.add_argument("--ar", choices=["peer", "nccl"], default="peer",
+                    help="row-parallel all-reduce at N > 1: one-shot over peer memory, or NCCL")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
@@ -256,6 +258,13 @@ def main():
     # ---------------- decode stack (the headline)
     st = stack.build_stack(model, a.layers, rank, world, dev, group=pg)
     torch.cuda.synchronize()
+    # row-parallel all-reduce: one-shot exchange over NVLink peer memory (k_allreduce.cu)
+    # for decode-sized messages, validated at setup (NCCL if the peer mapping fails)
+    ar_impl = "none (1 rank)"
+    if world > 1:
+        ar_impl = "nccl"
+        if a.ar == "peer":
+            ar_impl = stack.attach_peer_allreduce(st, max(ms) * model.hidden, dev)
     # inference: the quantized weights are resident and never written while the GEMMs
     # run, so the decode kernel may stream them ahead of the previous kernel (PDL)
     sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
@@ -512,6 +521,7 @@ def main():
             "config": {"workload": "codellama-34b-w4a16-linear-stack-decode", "layers": a.layers,
                        "decode_m": ms, "group": 128, "linears": [s.name for s in st.shards],
                        "parallelism": f"tp{world}" if world > 1 else "none",
+                       "allreduce": ar_impl,
                        "weights_bytes_per_step_all_ranks": bytes_all,
                        "l2": "no flush: every pass streams the stack's weights (GBs) > 126 MB L2",
                        "cuda_graph": used_graph, **launch_opts},

@@ -15,7 +15,9 @@ from . import sq
 
 class PeerAllReduce:
     """Row-parallel all-reduce of up to n_max fp16/bf16 outputs per call, one instance per
-    process group.  Collective construction (every rank of `group` must build it)."""
+    process group.  Collective construction (every rank of `group` must build it); a rank
+    whose mapping fails raises after the exchange, so callers agree on success with one
+    more collective (stack.attach_peer_allreduce) before the first call."""
 
     def __init__(self, n_max: int, device, group=None):
         self.group = group
@@ -26,9 +28,14 @@ class PeerAllReduce:
         self.buf = torch.zeros(nb, dtype=torch.uint8, device=device)  # flags must start at 0
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         torch.cuda.synchronize(device)
-        handle, off = sq.ipc_get_handle(self.buf)
+        try:
+            mine = sq.ipc_get_handle(self.buf)
+        except Exception:
+            mine = None  # still join the exchange, so no rank is left waiting in it
         allh = [None] * self.world
-        dist.all_gather_object(allh, (handle, off), group=group)
+        dist.all_gather_object(allh, mine, group=group)
+        if any(h is None for h in allh):
+            raise RuntimeError("PeerAllReduce: a rank could not export its buffer")
         self._opened = []
         addrs = []
         for q, (h, o) in enumerate(allh):
@@ -39,7 +46,6 @@ class PeerAllReduce:
                 self._opened.append(base)
                 addrs.append(base + o)
         self.peers = torch.tensor(addrs, dtype=torch.int64, device=device)
-        dist.barrier(group=group)
 
     def __call__(self, y: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """In place by default: y (this rank's partial) becomes the sum over ranks.  The epoch

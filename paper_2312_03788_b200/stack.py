@@ -31,6 +31,7 @@ class LinearStack:
     layers: list = field(default_factory=list)   # list[list[Linear]]
     group: object = None                          # torch.distributed process group (None: no AR)
     dtype: torch.dtype = torch.float16
+    peer_ar: object = None                        # peer.PeerAllReduce (None: NCCL all_reduce)
 
     @property
     def shards(self) -> list[LinearShard]:
@@ -105,7 +106,11 @@ def run_pass(st: LinearStack, buf: PassBuffers, path: int = sq.SQ_PATH_AUTO, wor
             sq.w4a16_gemm(buf.x[lin.shard.name], lin.q, out=y, path=path, workspace=workspace)
             n += 1
             if lin.shard.allreduce and st.group is not None:
-                dist.all_reduce(y, group=st.group)
+                if st.peer_ar is not None and y.numel() <= st.peer_ar.n_max:
+                    st.peer_ar(y)  # one-shot exchange over peer memory (k_allreduce.cu)
+                    n += 1
+                else:
+                    dist.all_reduce(y, group=st.group)
     return n
 
 
@@ -116,3 +121,34 @@ def pass_bytes(st: LinearStack, M: int) -> int:
 
 def pass_flops(st: LinearStack, M: int) -> int:
     return len(st.layers) * sum(gemm_flops(M, sh.K, sh.N) for sh in st.shards)
+
+
+def attach_peer_allreduce(st: LinearStack, n_max: int, device="cuda") -> str:
+    """Use the one-shot peer-memory all-reduce for the row-parallel
+    layers of messages up to n_max outputs (decode sizes), NCCL above.  Collective.  The
+    path is validated once with known data; if the IPC mapping or the exchange fails the
+    stack keeps NCCL and the reason is returned (plumbing choice, reported by bench.py)."""
+    import torch.distributed as dist
+
+    from . import peer
+
+    def agree(flag: bool) -> bool:
+        t = torch.tensor([1 if flag else 0], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=st.group)
+        return int(t.item()) == 1
+
+    ar, why = None, ""
+    try:
+        ar = peer.PeerAllReduce(n_max, device, group=st.group)
+    except Exception as e:  # IPC not permitted etc.
+        why = f"{type(e).__name__}: {e}"
+    if not agree(ar is not None):
+        return f"nccl (peer setup failed: {why or 'on another rank'})"[:200]
+    y = torch.full((4096,), float(st.rank + 1), dtype=st.dtype, device=device)
+    ar(y)
+    torch.cuda.synchronize()
+    want = float(st.world * (st.world + 1) // 2)
+    if not agree((not ar.failed()) and bool((y.float() == want).all())):
+        return "nccl (peer all-reduce validation failed)"
+    st.peer_ar = ar
+    return "peer-oneshot"
