@@ -177,12 +177,21 @@ int main(int argc, char** argv) {
   }
   auto encf = enc();
   struct Cfg { int mode, BN, GPS, occ, ns, hold; };
-  const int holds[] = {0, 500, 1000, 1500};
   Cfg cfgs[64]; int nc = 0;
-  for (int h : holds) {
-    for (int ns : {3, 4, 6}) cfgs[nc++] = {0, 64, 4, 2, ns, h};
-    cfgs[nc++] = {0, 64, 4, 1, 12, h};
-    cfgs[nc++] = {1, 64, 4, 2, 6, h};
+  if (argc > 1 && !strcmp(argv[1], "prefill")) {
+    // the prefill codes ring: one group per box (64-B rows) vs several groups per box
+    cfgs[nc++] = {0, 128, 1, 1, 12, 0};
+    cfgs[nc++] = {0, 128, 1, 1, 24, 0};
+    cfgs[nc++] = {0, 128, 2, 1, 12, 0};
+    cfgs[nc++] = {0, 128, 4, 1, 6, 0};
+    cfgs[nc++] = {0, 64, 4, 2, 4, 0};
+  } else {
+    const int holds[] = {0, 500, 1000, 1500};
+    for (int h : holds) {
+      for (int ns : {3, 4, 6}) cfgs[nc++] = {0, 64, 4, 2, ns, h};
+      cfgs[nc++] = {0, 64, 4, 1, 12, h};
+      cfgs[nc++] = {1, 64, 4, 2, 6, h};
+    }
   }
   for (int ci = 0; ci < nc; ++ci) {
     Cfg cf = cfgs[ci];
@@ -199,7 +208,7 @@ int main(int argc, char** argv) {
     const int STAGE = 64 * cf.BN * cf.GPS;
     const int smem = cf.ns * STAGE + 1024;
     void (*kp)(CUtensorMap, const uint8_t*, int, int, int, int, int, long long, uint32_t*, int) =
-        cf.ns == 3 ? k_ring<3> : cf.ns == 4 ? k_ring<4> : cf.ns == 6 ? k_ring<6> : k_ring<12>;
+        cf.ns == 3 ? k_ring<3> : cf.ns == 4 ? k_ring<4> : cf.ns == 6 ? k_ring<6> : cf.ns == 12 ? k_ring<12> : k_ring<24>;
     CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     snprintf(nm, sizeof nm, "%s BN=%d GPS=%d (%d KB) NS=%d occ=%d hold=%d", cf.mode ? "bulk" : "tma3", cf.BN, cf.GPS,
              STAGE / 1024, cf.ns, cf.occ, cf.hold);
