@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--skip-prefill", action="store_true")
     ap.add_argument("--skip-quant", action="store_true")
     ap.add_argument("--skip-calib", action="store_true")
+    ap.add_argument("--skip-7b", action="store_true")
     ap.add_argument("--ar", choices=["peer", "nccl"], default="peer",
                     help="row-parallel all-reduce at N > 1: one-shot over peer memory, or NCCL")
     ap.add_argument("--skip-e2e", action="store_true")
@@ -365,6 +366,48 @@ def main():
                            "frac_hbm": bm / tm / 1e9 / hbm_peak / world}
         del g2
 
+    # ---------------- BASELINE.json configs[1]: Code Llama-7B decode shapes on 1 GPU
+    cfg7 = None
+    if world == 1 and not a.skip_7b:
+        m7 = tp.CODELLAMA_7B
+        st7 = stack.build_stack(m7, m7.layers, 0, 1, dev)
+        per7, tot_b, tot_t = {}, 0.0, 0.0
+        for M in ms:
+            b7 = stack.make_buffers(st7, M, dev)
+            g7 = None
+            if not a.no_graph:
+                stack.run_pass(st7, b7)
+                torch.cuda.synchronize()
+                g7 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g7):
+                    stack.run_pass(st7, b7)
+
+            def one7(b7=b7, g7=g7):
+                g7.replay() if g7 is not None else stack.run_pass(st7, b7)
+
+            for _ in range(2):
+                one7()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, a.steps // 3)
+            e0.record()
+            for _ in range(reps):
+                one7()
+            e1.record()
+            torch.cuda.synchronize()
+            tm = e0.elapsed_time(e1) * 1e-3 / reps
+            bm = float(stack.pass_bytes(st7, M))
+            per7[str(M)] = {"ms_per_pass": tm * 1e3, "GB/s": bm / tm / 1e9, "frac_hbm": bm / tm / 1e9 / hbm_peak}
+            tot_b += bm
+            tot_t += tm
+            del g7, b7
+        cfg7 = {"workload": "codellama-7b-w4a16-linear-stack-decode (BASELINE.json configs[1])",
+                "layers": m7.layers, "linears": [s_.name for s_ in st7.shards],
+                "shapes_KxN": [[s_.K, s_.N] for s_ in st7.shards], "value": tot_b / tot_t / 1e9,
+                "unit": "GB/s", "frac_hbm": tot_b / tot_t / 1e9 / hbm_peak, "per_m": per7}
+        del st7
+        torch.cuda.empty_cache()
+
     # ---------------- end to end through the public API (host buffers)
     e2e = None
     if not a.skip_e2e:
@@ -532,6 +575,7 @@ def main():
             "prefill": prefill,
             "quantize": quant,
             "calibration": calib_res,
+            "codellama_7b_decode": cfg7,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
