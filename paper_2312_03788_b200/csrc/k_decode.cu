@@ -874,19 +874,29 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
                      void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
   const int slots = num_sms() * CT;
-  const double u64 = rowblock_utilization(N, 64, slots), u32 = rowblock_utilization(N, 32, slots);
-  // AUTO: whole row blocks when they balance (>= 85 % of the slots busy) AND a stream-K
-  // CTA would stream so little (< 160 KB of codes) that its fixed cost -- the fixup round
-  // trips at the end of the kernel -- dominates; measured crossover on the 34B shapes
-  // (o_proj 8192 x 8192 takes row blocks, down_proj 8192 x 22016 stays stream-K).
+  // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
+  // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots AND a CTA's
+  // row block exceeds the stream-K share by at most what the fixups cost (~2.5 µs at a CTA's
+  // ~19 GB/s: 44 KB of codes).  The shorter qualifying row height (more CTAs busy) wins.
+  // 34B o_proj 8192 x 8192 (+15 KB) and 7B qkv 4096 x 12288 (+43 KB) / o_proj 4096 x 4096
+  // (+36 KB) take row blocks; 34B qkv (+114 KB), down (+47 KB) and the rest stay stream-K.
+  const int G = K / kGroup;
   const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
-      (double)((N + 63) / 64) * ((K / kGroup + GPS - 1) / GPS));
-  bool dp = false;
+      (double)((N + 63) / 64) * ((G + GPS - 1) / GPS));
+  bool dp = sched == SQ_SCHED_ROWBLOCK;
   int bn = 64;
-  if (sched == SQ_SCHED_ROWBLOCK ||
-      (sched == SQ_SCHED_AUTO && std::max(u64, u32) >= 0.85 && sk_bytes_per_cta < 160.0 * 1024)) {
-    dp = true;
-    bn = u64 >= u32 ? 64 : 32;
+  if (sched == SQ_SCHED_ROWBLOCK) {
+    bn = rowblock_utilization(N, 64, slots) >= rowblock_utilization(N, 32, slots) ? 64 : 32;
+  } else if (sched == SQ_SCHED_AUTO) {
+    for (int cand : {32, 64}) {
+      const int rbs = (N + cand - 1) / cand;
+      const double rb_bytes = (double)cand * K / 2;
+      if (rbs <= slots && rb_bytes - sk_bytes_per_cta <= 44.0 * 1024) {
+        dp = true;
+        bn = cand;
+        break;
+      }
+    }
   }
   if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
   return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
