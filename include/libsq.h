@@ -243,6 +243,26 @@ SQ_API sq_status sq_allreduce_oneshot(const void* y_local, int dtype, void* y_ou
                                int* error_flag, void* stream);
 
 /*
+ * Row-parallel W4A16 linear + all-reduce in ONE kernel (decode, M <= sq_decode_max_m()):
+ * the decode GEMM's epilogue pushes every row block it finalizes straight into slot
+ * [rank] of every rank's symmetric buffer (the sq_allreduce_oneshot layout, one flag per
+ * row block), and after a CTA has pushed all of its row blocks it waits for the other
+ * ranks' copies of them and writes the rank-ordered fp32 sum to Y -- so Y (local) ends up
+ * bit-identical on every rank, and no partial is written to or re-read from local HBM.
+ * For M > sq_decode_max_m() (prefill) this is sq_w4a16_gemm followed by
+ * sq_allreduce_oneshot on Y.  Arguments: those of sq_w4a16_gemm (X is this rank's input
+ * shard [M][K_r], Wq/scales/zeros its row-parallel weight shard) plus those of
+ * sq_allreduce_oneshot with n_max >= M*N.  A buffer serves either this call or
+ * sq_allreduce_oneshot calls, in the same epoch mode, in one stream order on every rank.
+ */
+SQ_API sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype,
+                                  const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                                  void* Y, int64_t M, int64_t N, int64_t K, int group,
+                                  void* workspace, size_t workspace_bytes,
+                                  void* const* peer_bufs, int rank, int world, int64_t n_max,
+                                  uint32_t epoch, int* error_flag, void* stream);
+
+/*
  * CUDA IPC plumbing for the symmetric buffers (host calls, no stream work).
  * sq_ipc_get_handle: export the cudaMalloc block containing dev_ptr into handle_out
  * (sq_ipc_handle_bytes() bytes) and report dev_ptr's byte offset inside that block (a

@@ -347,16 +347,28 @@ struct Sched {
 };
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// Row-parallel all-reduce fused into the epilogue (sq_w4a16_gemm_allreduce; the buffer
+// layout and protocol are those of k_allreduce.cu: header, flags[2][world][kArMaxChunks],
+// fp16/bf16 slots[2][world][n_max]; here a "chunk" is a row block).  world == 0: off.
+constexpr size_t kArHdr = 128;
+__device__ __forceinline__ uint32_t* ar_flags(uint8_t* base, int world, int par) {
+  return reinterpret_cast<uint32_t*>(base + kArHdr) + (size_t)par * world * kArMaxChunks;
+}
+__device__ __forceinline__ uint16_t* ar_slots(uint8_t* base, int world, int par, int q, int64_t n_max) {
+  return reinterpret_cast<uint16_t*>(base + kArHdr + (size_t)2 * world * kArMaxChunks * sizeof(uint32_t)) +
+         ((size_t)par * world + q) * n_max;
+}
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-template <int MT, bool kBF16, int BN, int XR, int CT>
+template <int MT, bool kBF16, int BN, int XR, int CT, bool kAR>
 __global__ void __launch_bounds__(kThreads, CT)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
-              int M, int N, Work wk, int early_weights) {
+              int M, int N, Work wk, int early_weights, const ArParams ar) {
   using C = Cfg<MT, BN, XR, CT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -455,6 +467,49 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     int s = 0;
     uint32_t redph = 0;                   // phase bit per stage
     bool waited = false;
+    // fused all-reduce: this CTA's finalized row blocks are pushed to every rank as they
+    // complete and reduced after the CTA has pushed all of them (waiting only at the end
+    // keeps the cross-GPU waits acyclic)
+    __shared__ int fin_list[64];
+    int n_fin = 0;
+    uint32_t epoch = ar.epoch;
+    if (kAR && epoch == 0) {
+      const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(ar.peers[ar.rank]);
+      epoch = cur == 0xFFFFFFFFu ? 2u : cur + 1u;
+    }
+    const int par = epoch & 1;
+    auto emit = [&](int rb, const float (&val)[E]) {  // final values of row block rb
+      const int n0 = rb * BN;
+      if (!kAR) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+          if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(val[i]);
+        }
+        return;
+      }
+      for (int p = 0; p < ar.world; ++p) {
+        uint16_t* dst = ar_slots(ar.peers[p], ar.world, par, ar.rank, ar.n_max);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+          if (t < M && n0 + row < N) dst[(size_t)t * N + n0 + row] = to_out(val[i]);
+        }
+      }
+      __threadfence_system();
+      __syncwarp();
+      if (lane < ar.world) {
+        uint32_t* f = ar_flags(ar.peers[lane], ar.world, par) + (size_t)ar.rank * kArMaxChunks + rb;
+        asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(f), "r"(epoch) : "memory");
+      }
+      if (n_fin < 64) {
+        if (lane == 0) fin_list[n_fin] = rb;
+      } else if (lane == 0) {
+        atomicExch(ar.err, 2);  // more finalized row blocks than the list holds
+      }
+      ++n_fin;
+      __syncwarp();
+    };
     for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
       const int rb = sc.u / wk.upb;
       if (sc.range_last()) {
@@ -479,11 +534,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         if (SQ_DEC_ABLATE == 8) {
           if (v[0] == 1234.5f) Y[0] = 1;
         } else if (sc.full) {
-#pragma unroll
-          for (int i = 0; i < E; ++i) {
-            const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
-            if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(v[i]);
-          }
+          emit(rb, v);
         } else if (SQ_DEC_ABLATE == 16) {
           if (v[0] == 1234.5f) Y[0] = 1;
         } else {
@@ -522,16 +573,60 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 #pragma unroll
               for (int i = 0; i < E; ++i) tot[i] += part[i];
             }
-#pragma unroll
-            for (int i = 0; i < E; ++i) {
-              const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
-              if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(tot[i]);
-            }
+            emit(rb, tot);
             if (lane == 0) counters[rb] = 0;  // leave the workspace zeroed
           }
         }
       }
       if (++s == C::NS) s = 0;
+    }
+    if (kAR) {
+      // reduce the row blocks this CTA finalized: wait for every rank's copy (bounded),
+      // sum in rank order in fp32 (bit-identical Y on every rank), store
+      const int nf = n_fin < 64 ? n_fin : 64;
+      bool timed_out = false;
+      for (int f = 0; f < nf && !timed_out; ++f) {
+        const int rb = fin_list[f], n0 = rb * BN;
+        if (lane < ar.world) {
+          const uint32_t* fl = ar_flags(ar.peers[ar.rank], ar.world, par) + (size_t)lane * kArMaxChunks + rb;
+          uint32_t v, polls = 0;
+          while (true) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(fl) : "memory");
+            if (v == epoch) break;
+            if (++polls > (1u << 24)) {
+              atomicExch(ar.err, 1);
+              break;
+            }
+            if (polls > 64) __nanosleep(polls > 4096 ? 1000 : 64);
+          }
+          if (v != epoch) timed_out = true;
+        }
+        timed_out = __any_sync(0xffffffffu, timed_out);
+        if (timed_out) break;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+          if (t < M && n0 + row < N) {
+            float acc = 0.0f;
+            for (int q = 0; q < ar.world; ++q) {
+              const uint16_t b = __ldcv(ar_slots(ar.peers[ar.rank], ar.world, par, q, ar.n_max) +
+                                        (size_t)t * N + n0 + row);
+              acc += kBF16 ? __bfloat162float(__ushort_as_bfloat16(b)) : __half2float(__ushort_as_half(b));
+            }
+            Y[(size_t)t * N + n0 + row] = to_out(acc);
+          }
+        }
+      }
+      // the last CTA to finish advances the device-managed epoch
+      if (ar.epoch == 0 && lane == 0) {
+        uint32_t* hdr = reinterpret_cast<uint32_t*>(ar.peers[ar.rank]);
+        __threadfence();
+        if (atomicAdd(hdr + 1, 1u) == gridDim.x - 1) {
+          hdr[1] = 0;
+          __threadfence();
+          *reinterpret_cast<volatile uint32_t*>(hdr) = epoch;
+        }
+      }
     }
 #if SQ_DEC_TRACE
     if (lane == 0 && tr_row) tr_row[3] = gtime();
@@ -790,9 +885,11 @@ int ctas_per_sm() {
   static int cached = -1;
   if (cached < 0) {
     int n = 0;
-    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT>, kThreads,
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT, false>, kThreads,
                                                       Cfg<MT, BN, XR, CT>::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
     cached = std::min(n, CT);
@@ -802,7 +899,8 @@ int ctas_per_sm() {
 
 template <int MT, bool kBF16, int BN, int XR, int CT>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                     void* Y, int M, int N, int K, void* ws, bool dp, cudaStream_t st, const char** why) {
+                     void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, cudaStream_t st,
+                     const char** why) {
   using C = Cfg<MT, BN, XR, CT>;
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
@@ -858,8 +956,11 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT>, tw, tx, ts, tz, (uint16_t*)Y, counters,
-                            partials, M, N, wk, early);
+  if (ar.world > 0)
+    return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, true>, tw, tx, ts, tz, (uint16_t*)Y,
+                              counters, partials, M, N, wk, early, ar);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, false>, tw, tx, ts, tz, (uint16_t*)Y, counters,
+                            partials, M, N, wk, early, ar);
 }
 
 // Fraction of the resident CTA slots kept busy by whole row blocks of height bn.
@@ -871,7 +972,8 @@ double rowblock_utilization(int N, int bn, int slots) {
 
 template <int MT, bool kBF16, int XR, int CT>
 cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                     void* Y, int M, int N, int K, void* ws, cudaStream_t st, const char** why) {
+                     void* Y, int M, int N, int K, void* ws, const ArParams& ar, cudaStream_t st,
+                     const char** why) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
   const int slots = num_sms() * CT;
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
@@ -898,8 +1000,8 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
       }
     }
   }
-  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
-  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, st, why);
+  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
+  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
 }
 
 }  // namespace
@@ -915,17 +1017,18 @@ size_t decode_workspace_bytes(int64_t N) {
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
-                          cudaStream_t st, const char** why) {
+                          cudaStream_t st, const char** why, const ArParams* ar_in) {
+  const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
   constexpr int C2 = SQ_DEC_CTAS, C1 = SQ_DEC_CTAS_M1;
   if (M == 1)  // batch-1 decode: stage one activation row, smaller stages, more CTAs per SM
-    return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-                : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+    return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+                : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
   if (M <= 8)
-    return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-                : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
-  return bf16 ? launch_m<2, true, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why)
-              : launch_m<2, false, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, st, why);
+    return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+                : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+  return bf16 ? launch_m<2, true, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+              : launch_m<2, false, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
 }
 
 }  // namespace sq

@@ -250,6 +250,45 @@ sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, dou
                      "sq_sq_diff_sum");
 }
 
+sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                                  const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K, int group,
+                                  void* workspace, size_t workspace_bytes, void* const* peer_bufs, int rank,
+                                  int world, int64_t n_max, uint32_t epoch, int* error_flag, void* stream) {
+  g_last_error.clear();
+  if (world <= 0 || rank < 0 || rank >= world || M < 0 || N <= 0 || M * N > n_max)
+    return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm_allreduce: M=%lld N=%lld n_max=%lld rank=%d world=%d", (long long)M,
+                (long long)N, (long long)n_max, rank, world);
+  if ((n_max + ar_chunk_elems() - 1) / ar_chunk_elems() > kArMaxChunks || (N + 31) / 32 > kArMaxChunks)
+    return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: n_max or N too large");
+  if (M == 0) return SQ_OK;
+  if (!peer_bufs || !error_flag) return fail(SQ_ERR_NULL, "sq_w4a16_gemm_allreduce: null pointer");
+  if (!aligned16(peer_bufs) || n_max % 8 != 0)
+    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: unaligned peer array or n_max %% 8 != 0");
+  if (M > kDecodeMaxM || g_opt_decode_kernel != SQ_DECK_MMA_SYNC) {
+    // prefill-sized (or tcgen05 decode): the GEMM, then the one-shot exchange kernel (PDL)
+    sq_status st = sq_w4a16_gemm(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace, workspace_bytes,
+                                 stream);
+    if (st != SQ_OK) return st;
+    return sq_allreduce_oneshot(Y, x_dtype, Y, M * N, n_max, peer_bufs, rank, world, epoch, error_flag, stream);
+  }
+  // decode: one kernel -- the epilogue pushes each finished row block to every rank and
+  // reduces its own row blocks once every rank's copy has arrived
+  if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm_allreduce: null pointer");
+  if (K <= 0 || group != 128 || K % group != 0 || !valid_dtype(x_dtype))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
+  if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) || !aligned16(Y))
+    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: N %% 8 != 0 or unaligned pointer");
+  const size_t need = decode_workspace_bytes(N);
+  if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
+    return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm_allreduce: decode needs %zu workspace bytes", need);
+  const ArParams ar{reinterpret_cast<uint8_t* const*>(peer_bufs), n_max, error_flag, rank, world, epoch};
+  const char* why = nullptr;
+  cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace,
+                                (cudaStream_t)stream, &why, &ar);
+  if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: %s", why);
+  return cuda_status(e, "sq_w4a16_gemm_allreduce");
+}
+
 size_t sq_allreduce_buffer_bytes(int64_t n_max, int world) {
   if (n_max <= 0 || world <= 0) return 0;
   return ar_buffer_bytes(n_max, world);

@@ -37,9 +37,17 @@ inline size_t counter_region_bytes(int64_t counters) {
 }
 bool prefill_streamk(int64_t M, int64_t N, int64_t K);
 size_t decode_workspace_bytes(int64_t N);
+// Row-parallel all-reduce fused into the decode epilogue (world == 0: plain GEMM).
+struct ArParams {
+  uint8_t* const* peers;  // device array of `world` symmetric-buffer addresses
+  int64_t n_max;
+  int* err;
+  int rank, world;
+  uint32_t epoch;  // 0: device-managed
+};
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
-                          cudaStream_t st, const char** why);
+                          cudaStream_t st, const char** why, const ArParams* ar = nullptr);
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,

@@ -64,3 +64,13 @@ class PeerAllReduce:
         for base in self._opened:
             sq.ipc_close(base)
         self._opened = []
+
+    def gemm(self, X: torch.Tensor, q: sq.QuantizedLinear, out: torch.Tensor | None = None,
+             workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Row-parallel linear + all-reduce in one call (sq_w4a16_gemm_allreduce): X is this
+        rank's input shard, q its weight shard; returns the summed Y on every rank."""
+        if X.shape[0] * q.N > self.n_max:
+            raise ValueError(f"PeerAllReduce.gemm: {X.shape[0] * q.N} outputs > n_max {self.n_max}")
+        return sq.w4a16_gemm_allreduce(X, q, self.peers, self.rank, self.world, self.n_max, self.err,
+                                       out=out, workspace=workspace, stream=stream)
+

@@ -67,6 +67,8 @@ def _load():
         "sq_sq_diff_sum_workspace_bytes": (sz, []),
         "sq_sq_diff_sum": (i32, [vp, vp, i32, i64, vp, vp, sz, vp]),
         "sq_allreduce_buffer_bytes": (sz, [i64, i32]),
+        "sq_w4a16_gemm_allreduce": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp, i32, i32, i64,
+                                          c.c_uint32, vp, vp]),
         "sq_allreduce_oneshot": (i32, [vp, i32, vp, i64, i64, vp, i32, i32, c.c_uint32, vp, vp]),
         "sq_ipc_handle_bytes": (sz, []),
         "sq_ipc_get_handle": (i32, [vp, vp, c.POINTER(sz)]),
@@ -86,7 +88,7 @@ EXPORTED = (
     "sq_get_option", "sq_act_absmax",
     "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
     "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
-    "sq_sq_diff_sum", "sq_allreduce_buffer_bytes", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
+    "sq_sq_diff_sum", "sq_allreduce_buffer_bytes", "sq_w4a16_gemm_allreduce", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
     "sq_ipc_get_handle", "sq_ipc_open_handle", "sq_ipc_close",
 )
 
@@ -300,3 +302,27 @@ def ipc_open_handle(handle: bytes) -> int:
 
 def ipc_close(addr: int) -> None:
     _check(_load().sq_ipc_close(ctypes.c_void_p(addr)))
+
+
+def w4a16_gemm_allreduce(X: torch.Tensor, q: QuantizedLinear, peers_dev: torch.Tensor, rank: int, world: int,
+                         n_max: int, error_flag: torch.Tensor, epoch: int = 0, out: torch.Tensor | None = None,
+                         workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Row-parallel W4A16 linear + all-reduce over peer memory: Y = sum over ranks of
+    X_r · dequant(q_r)^T, identical on every rank (sq_w4a16_gemm_allreduce; one kernel for
+    decode sizes)."""
+    _need_cuda(X, out, workspace, peers_dev, error_flag)
+    M, K = X.shape
+    if K != q.K:
+        raise ValueError(f"K mismatch: X has {K}, weight has {q.K}")
+    if out is None:
+        out = torch.empty((M, q.N), dtype=X.dtype, device=X.device)
+    if workspace is None:
+        need = w4a16_gemm_workspace_bytes(M, q.N, K, q.group)
+        if need:
+            workspace = default_workspace(X.device, need)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(_load().sq_w4a16_gemm_allreduce(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
+                                           _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes,
+                                           _ptr(peers_dev), int(rank), int(world), int(n_max),
+                                           ctypes.c_uint32(epoch & 0xFFFFFFFF), _ptr(error_flag), _stream(stream)))
+    return out

@@ -103,14 +103,18 @@ def run_pass(st: LinearStack, buf: PassBuffers, path: int = sq.SQ_PATH_AUTO, wor
     for row in st.layers:
         for lin in row:
             y = buf.y[lin.shard.name]
+            fused = (lin.shard.allreduce and st.group is not None and st.peer_ar is not None
+                     and y.numel() <= st.peer_ar.n_max and path == sq.SQ_PATH_AUTO)
+            if fused:
+                # row-parallel linear + all-reduce over peer memory: one kernel at decode
+                # sizes (sq_w4a16_gemm_allreduce), GEMM + one-shot exchange kernel above
+                st.peer_ar.gemm(buf.x[lin.shard.name], lin.q, out=y, workspace=workspace)
+                n += 1 if buf.M <= sq.decode_max_m() else 2
+                continue
             sq.w4a16_gemm(buf.x[lin.shard.name], lin.q, out=y, path=path, workspace=workspace)
             n += 1
             if lin.shard.allreduce and st.group is not None:
-                if st.peer_ar is not None and y.numel() <= st.peer_ar.n_max:
-                    st.peer_ar(y)  # one-shot exchange over peer memory (k_allreduce.cu)
-                    n += 1
-                else:
-                    dist.all_reduce(y, group=st.group)
+                dist.all_reduce(y, group=st.group)
     return n
 
 

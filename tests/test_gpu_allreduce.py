@@ -77,6 +77,45 @@ def test_oneshot_in_place_and_timeout():
     assert int(err.item()) == 1
 
 
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("M", [1, 5, 16])
+@pytest.mark.parametrize("N,K", [(1024, 1024), (2048, 2048), (1024, 3072)])
+def test_fused_gemm_allreduce_streams(M, N, K, dtype):
+    """sq_w4a16_gemm_allreduce (decode: one kernel) for two ranks on two streams of one GPU
+    (grids of <= 148 CTAs, so both kernels are resident together): every rank's Y equals the
+    rank-ordered fp32 sum of the two ranks' plain sq_w4a16_gemm partials, bit for bit, over
+    back-to-back calls (both epoch parities, device-managed epoch)."""
+    from paper_2312_03788_b200 import synth, tp
+
+    world = 2
+    W = torch.from_numpy(synth.weights(N, K, seed=N + K)).to(DEV)
+    ranges = tp.channel_split(K, world)
+    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()) for a, b in ranges]
+    n_max = M * N
+    nb = sq.allreduce_buffer_bytes(n_max, world)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    errs = [torch.zeros(1, dtype=torch.int32, device=DEV) for _ in range(world)]
+    wss = [torch.zeros(sq.w4a16_gemm_workspace_bytes(M, N, K), dtype=torch.uint8, device=DEV) for _ in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
+    for it in range(4):
+        X = (torch.randn(M, K, generator=g, device=DEV) * 2).to(dtype)
+        xs = [X[:, a:b].contiguous() for a, b in ranges]
+        parts = [sq.w4a16_gemm(xs[r], qs[r]) for r in range(world)]
+        outs = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                sq.w4a16_gemm_allreduce(xs[r], qs[r], peers, r, world, n_max, errs[r], out=outs[r],
+                                        workspace=wss[r], stream=streams[r])
+        torch.cuda.synchronize()
+        assert all(int(e.item()) == 0 for e in errs)
+        want = _expected(parts)
+        for r in range(world):
+            assert torch.equal(outs[r].view(torch.int16), want.view(torch.int16)), (it, r)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -137,6 +176,22 @@ def _worker(rank, world, port, q):
             y_ref = oracle.gemm(X, full["Wq"], full["scales"], full["zeros"])
             err = np.linalg.norm(y.float().cpu().double().numpy() - y_ref) / np.linalg.norm(y_ref)
             ok.append(bool(err <= 2e-3))
+        # the fused row-parallel linear (one kernel at decode sizes) on the same buffers
+        for i, (name, K, N) in enumerate(tp.full_shapes(model)):
+            sh = tp.layer_shards(model, rank, world)[i]
+            if sh.kind != "row":
+                continue
+            W = synth.weights(N, K, seed=20 + i)
+            k0, k1 = sh.k_range
+            qsh = sq.quantize_pack_groupwise(torch.from_numpy(np.ascontiguousarray(W[:, k0:k1])).to(DEV))
+            full = oracle.quantize_pack(W, None)
+            for M in (1, 16, 40):  # 40: prefill GEMM + exchange kernel
+                X = synth.activations(M, K, seed=50 + i + M).astype(np.float16)
+                y = ar.gemm(torch.from_numpy(np.ascontiguousarray(X[:, k0:k1])).to(DEV), qsh)
+                torch.cuda.synchronize()
+                y_ref = oracle.gemm(X, full["Wq"], full["scales"], full["zeros"])
+                err = np.linalg.norm(y.float().cpu().double().numpy() - y_ref) / np.linalg.norm(y_ref)
+                ok.append(bool(err <= 2e-3))
         ok.append(not ar.failed())
         ar.close()
         q.put((rank, all(ok)))
