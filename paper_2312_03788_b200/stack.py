@@ -155,4 +155,4 @@ def attach_peer_allreduce(st: LinearStack, n_max: int, device="cuda") -> str:
     if not agree((not ar.failed()) and bool((y.float() == want).all())):
         return "nccl (peer all-reduce validation failed)"
     st.peer_ar = ar
-    return "peer-oneshot"
+    return "peer: fused GEMM+all-reduce kernel (decode sizes) over NVLink peer memory"
