@@ -147,3 +147,20 @@ def test_allreduce_argument_errors(L):
     assert L.sq_ipc_get_handle(None, FAKE, None) == sq.SQ_ERR_NULL
     assert L.sq_ipc_open_handle(None, None) == sq.SQ_ERR_NULL
     assert L.sq_ipc_close(None) == sq.SQ_ERR_NULL
+
+
+def test_gemm_allreduce_argument_errors(L):
+    """sq_w4a16_gemm_allreduce validates on the host before any launch."""
+    f = L.sq_w4a16_gemm_allreduce
+
+    def call(M=4, N=256, K=512, rank=0, world=2, n_max=1024, peers=FAKE, err=FAKE, dt=0, g=128):
+        return f(FAKE, dt, FAKE, FAKE, FAKE, FAKE, M, N, K, g, FAKE, 1 << 20, peers, rank, world, n_max, 0, err, None)
+
+    assert call(n_max=512) == sq.SQ_ERR_SHAPE       # M*N > n_max
+    assert call(rank=2) == sq.SQ_ERR_SHAPE
+    assert call(world=0) == sq.SQ_ERR_SHAPE
+    assert call(peers=None) == sq.SQ_ERR_NULL
+    assert call(err=None) == sq.SQ_ERR_NULL
+    assert call(n_max=1028) == sq.SQ_ERR_ALIGN
+    assert call(g=64) == sq.SQ_ERR_UNSUPPORTED
+    assert call(M=0) == sq.SQ_OK
