@@ -71,14 +71,15 @@ constexpr int GPS = 4;          // groups per stage
 constexpr int kConsumerWarps = SQ_DEC_CW;
 constexpr int kRowSplit = kConsumerWarps / GPS;  // warps sharing one group's rows
 static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multiple of GPS");
-constexpr int kProducerWarp = kConsumerWarps;      // TMA
-constexpr int kEpilogueWarp = kConsumerWarps + 1;  // cross-warp sum, output / stream-K fixup
-constexpr int kThreads = (kConsumerWarps + 2) * 32;
+// warp roles (Cfg): consumers 0 .. CW-1, TMA producer CW, epilogue CW + 1
 #ifndef SQ_DEC_CTAS_M1
 #define SQ_DEC_CTAS_M1 2  // CTAs per SM of the M = 1 kernel (1-token activation box; 3 measured slower)
 #endif
+#ifndef SQ_DEC_CTAS_M16
+#define SQ_DEC_CTAS_M16 2  // M = 9..16; 1 = one CTA per SM, 128-row blocks, 8 consumer warps (measured 2-35 % slower)
+#endif
 constexpr int kMaxCtasPerSm = SQ_DEC_CTAS > SQ_DEC_CTAS_M1 ? SQ_DEC_CTAS : SQ_DEC_CTAS_M1;
-constexpr int kMaxBN = 64;      // row-block heights: 32 or 64
+constexpr int kMaxBN = 128;     // row-block heights: 32 or 64 (2 CTAs/SM), 128 (1 CTA/SM)
 constexpr int kMinBN = 32;
 
 // MT: 8-token MMA n-tiles; XR: token rows of the activation box actually staged (M = 1 stages
@@ -86,8 +87,12 @@ constexpr int kMinBN = 32;
 template <int MT, int BN, int XR, int CT>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
-  static constexpr int kSmemBudget = (CT <= 2 ? 112 : 74) * 1024;  // per CTA
-  static constexpr int RT = BN / 16 / kRowSplit;          // 16-row tiles per consumer warp
+  // one CTA per SM: 8 consumer warps (two per group, row split) over 128-row blocks
+  static constexpr int CW = CT == 1 ? 8 : kConsumerWarps;
+  static constexpr int RS = CW / GPS;
+  static constexpr int THREADS = (CW + 2) * 32;
+  static constexpr int kSmemBudget = (CT == 1 ? 220 : CT == 2 ? 112 : 74) * 1024;  // per CTA
+  static constexpr int RT = BN / 16 / RS;                 // 16-row tiles per consumer warp
   static_assert(RT >= 1, "row block too short for the consumer split");
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
   static constexpr int XB = GPS * XR * kGroup * 2;        // 1 / 8 / 16 KB
@@ -99,7 +104,12 @@ struct Cfg {
   // At a segment end each consumer warp parks its fp32 partial sums (MPAD x BN) over its
   // own group's activation slice of the stage, which only that warp reads.
   static constexpr int XSLICE = XB / GPS;
-  static_assert(XR * BN * 4 <= XSLICE, "partial-sum slot must fit the activation slice");
+  // partial sums are parked over the group's activation slice, or over its codes slab when
+  // the slice is too small (128-row blocks); both were fully read before the park
+  static constexpr bool kParkCodes = XR * BN * 4 > XSLICE;
+  static constexpr int PARK_OFF = kParkCodes ? 0 : CODES;
+  static constexpr int PARK_STRIDE = kParkCodes ? BN * 64 : XSLICE;
+  static_assert(XR * BN * 4 <= PARK_STRIDE, "partial-sum slot must fit");
   static_assert(XR * BN >= 32, "epilogue lanes");
   static constexpr int OFF_BAR = NS * STAGE;  // full[NS], empty[NS], red_full[NS]
   static constexpr int SMEM = OFF_BAR + 3 * NS * 8;
@@ -364,7 +374,7 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 
 template <int MT, bool kBF16, int BN, int XR, int CT, bool kAR>
-__global__ void __launch_bounds__(kThreads, CT)
+__global__ void __launch_bounds__(Cfg<MT, BN, XR, CT>::THREADS, CT)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
@@ -383,8 +393,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(bar_full + 8 * i, 1);
-      mbar_init(bar_empty + 8 * i, kConsumerWarps);
-      mbar_init(red_full + 8 * i, kConsumerWarps);
+      mbar_init(bar_empty + 8 * i, C::CW);
+      mbar_init(red_full + 8 * i, C::CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -407,7 +417,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
   // the next kernel in the stream may start its prologue as our CTAs retire
   pdl_launch_dependents();
 
-  if (warp == kProducerWarp) {
+  if (warp == C::CW) {  // producer
     // ===================== TMA producer =====================
     if (lane == 0) {
       prefetch_tmap(&tm_w);
@@ -458,7 +468,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     return __half_as_ushort(__float2half_rn(v));
   };
 
-  if (warp == kEpilogueWarp) {
+  if (warp == C::CW + 1) {  // epilogue
     // ===================== epilogue: one warp, off the consumers' critical path =====================
     // Walks the same schedule as the consumers.  At each segment end it sums the four
     // warps' parked partials (fixed warp order), hands the stage back to the producer,
@@ -515,8 +525,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       if (sc.range_last()) {
         mbar_wait_idle(red_full + 8 * s, (redph >> s) & 1u);
         redph ^= 1u << s;
-        const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODES);
-        constexpr int W = C::XSLICE / 4;  // floats per group slot
+        const float* sl = reinterpret_cast<const float*>(smem + s * C::STAGE + C::PARK_OFF);
+        constexpr int W = C::PARK_STRIDE / 4;  // floats per group slot
         float v[E];
 #pragma unroll
         for (int i = 0; i < E; ++i) {
@@ -525,7 +535,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive_cnt(bar_empty + 8 * s, kConsumerWarps);  // stage back to the producer
+        if (lane == 0) mbar_arrive_cnt(bar_empty + 8 * s, C::CW);  // stage back to the producer
         if (!waited) {  // global accesses below must follow the previous kernel (PDL)
           pdl_wait();
           waited = true;
@@ -634,9 +644,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     return;
   }
 
-  // ===== consumers: warp w = group (w % GPS), rows [roff, roff + BN / kRowSplit) of each stage =====
+  // ===== consumers: warp w = group (w % GPS), rows [roff, roff + BN / RS) of each stage =====
   const int r = lane / 4, j = lane % 4;
-  const int grp = warp % GPS, roff = (warp / GPS) * (BN / kRowSplit);
+  const int grp = warp % GPS, roff = (warp / GPS) * (BN / C::RS);
   float acc[C::RT][MT][4];
 #pragma unroll
   for (int rt = 0; rt < C::RT; ++rt)
@@ -822,9 +832,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       // them to the epilogue warp, which also releases the stage; no CTA-wide barrier
       // (the warps of one group write disjoint rows of the group's slot, after all of them
       // have read their activation fragments from it: named barrier 1 + grp)
-      if (kRowSplit > 1)
-        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * kRowSplit) : "memory");
-      float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::CODES + grp * C::XSLICE);
+      if (C::RS > 1)
+        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * C::RS) : "memory");
+      float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::PARK_OFF + grp * C::PARK_STRIDE);
 #pragma unroll
       for (int rt = 0; rt < C::RT; ++rt)
 #pragma unroll
@@ -889,7 +899,8 @@ int ctas_per_sm() {
                          Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
     cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT, false>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT, false>,
+                                                      Cfg<MT, BN, XR, CT>::THREADS,
                                                       Cfg<MT, BN, XR, CT>::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
     cached = std::min(n, CT);
@@ -947,7 +958,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)P, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_ALLOC;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -976,6 +987,11 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
                      const char** why) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
   const int slots = num_sms() * CT;
+  if constexpr (CT == 1) {  // one CTA per SM: 128-row blocks, stream-K
+    (void)sched;
+    (void)slots;
+    return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, st, why);
+  } else {
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
   // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots AND a CTA's
   // row block exceeds the stream-K share by at most what the fixups cost (~2.5 µs at a CTA's
@@ -1002,6 +1018,7 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   }
   if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
   return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
+  }
 }
 
 }  // namespace
@@ -1027,8 +1044,9 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   if (M <= 8)
     return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
                 : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
-  return bf16 ? launch_m<2, true, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-              : launch_m<2, false, 16, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+  constexpr int C16 = SQ_DEC_CTAS_M16;
+  return bf16 ? launch_m<2, true, 16, C16>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+              : launch_m<2, false, 16, C16>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
 }
 
 }  // namespace sq
