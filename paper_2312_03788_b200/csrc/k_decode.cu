@@ -993,11 +993,13 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, st, why);
   } else {
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
-  // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots AND a CTA's
+  // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots, a CTA's
   // row block exceeds the stream-K share by at most what the fixups cost (~2.5 µs at a CTA's
-  // ~19 GB/s: 44 KB of codes).  The shorter qualifying row height (more CTAs busy) wins.
-  // 34B o_proj 8192 x 8192 (+15 KB) and 7B qkv 4096 x 12288 (+43 KB) / o_proj 4096 x 4096
-  // (+36 KB) take row blocks; 34B qkv (+114 KB), down (+47 KB) and the rest stay stream-K.
+  // ~19 GB/s: 48 KB of codes), and the row block is short (<= 192 KB: longer ones stream
+  // below the HBM rate with fewer CTAs busy).  The shorter qualifying row height wins.
+  // 34B o_proj 8192 x 8192 (+15 KB, 128 KB), 7B qkv 4096 x 12288 (+46 KB, 128 KB) and 7B
+  // o_proj 4096 x 4096 (+36 KB, 64 KB) take row blocks; 34B qkv (+114 KB), 34B down_proj
+  // (+47 KB but 352 KB per CTA) and the rest stay stream-K.
   const int G = K / kGroup;
   const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
       (double)((N + 63) / 64) * ((G + GPS - 1) / GPS));
@@ -1009,7 +1011,7 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     for (int cand : {32, 64}) {
       const int rbs = (N + cand - 1) / cand;
       const double rb_bytes = (double)cand * K / 2;
-      if (rbs <= slots && rb_bytes - sk_bytes_per_cta <= 44.0 * 1024) {
+      if (rbs <= slots && rb_bytes - sk_bytes_per_cta <= 48.0 * 1024 && rb_bytes <= 192.0 * 1024) {
         dp = true;
         bn = cand;
         break;
