@@ -75,6 +75,9 @@ static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multi
 #ifndef SQ_DEC_CTAS_M1
 #define SQ_DEC_CTAS_M1 2  // CTAs per SM of the M = 1 kernel (1-token activation box; 3 measured slower)
 #endif
+#ifndef SQ_DEC_SK_BN
+#define SQ_DEC_SK_BN 0  // stream-K row-block height: 0 = by shape (AUTO), 32 / 64 forced
+#endif
 #ifndef SQ_DEC_CTAS_M16
 #define SQ_DEC_CTAS_M16 2  // M = 9..16; 1 = one CTA per SM, 128-row blocks, 8 consumer warps (measured 2-35 % slower)
 #endif
@@ -1004,7 +1007,10 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
       (double)((N + 63) / 64) * ((G + GPS - 1) / GPS));
   bool dp = sched == SQ_SCHED_ROWBLOCK;
-  int bn = 64;
+  // stream-K row-block height: 32 rows for M = 9..16 on layers below 48 MB of codes (half
+  // the cut row blocks' fixup work; measured -8..-13 % on the 7B shapes, +2 % on 34B qkv),
+  // 64 otherwise (larger stages stream faster)
+  int bn = SQ_DEC_SK_BN ? SQ_DEC_SK_BN : (MT == 2 && (double)N * K / 2 < 48.0 * 1024 * 1024 ? 32 : 64);
   if (sched == SQ_SCHED_ROWBLOCK) {
     bn = rowblock_utilization(N, 64, slots) >= rowblock_utilization(N, 32, slots) ? 64 : 32;
   } else if (sched == SQ_SCHED_AUTO) {
