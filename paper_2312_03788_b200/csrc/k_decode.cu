@@ -78,6 +78,9 @@ static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multi
 #ifndef SQ_DEC_SK_BN
 #define SQ_DEC_SK_BN 0  // stream-K row-block height: 0 = by shape (AUTO), 32 / 64 forced
 #endif
+#ifndef SQ_DEC_XR4
+#define SQ_DEC_XR4 0  // 1: M = 2..4 stage 4 activation rows instead of 8 (measured -3..+5 %, net ~0)
+#endif
 #ifndef SQ_DEC_CTAS_M16
 #define SQ_DEC_CTAS_M16 2  // M = 9..16; 1 = one CTA per SM, 128-row blocks, 8 consumer warps (measured 2-35 % slower)
 #endif
@@ -1049,6 +1052,11 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   if (M == 1)  // batch-1 decode: stage one activation row, smaller stages, more CTAs per SM
     return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
                 : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+#if SQ_DEC_XR4
+  if (M <= 4)  // stage four activation rows
+    return bf16 ? launch_m<1, true, 4, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+                : launch_m<1, false, 4, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+#endif
   if (M <= 8)
     return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
                 : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
