@@ -79,3 +79,40 @@ def test_fullsize_sampled_parity(name):
         y = Y.cpu().numpy()[np.ix_(toks, rows)].astype(np.float64)
         err = np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref)
         assert err <= 1e-3, (name, M, err)
+
+
+def test_fullsize_bf16_activations_and_large_m():
+    """bf16 activations at a full 34B shape (down_proj, K = 22016: 172 groups, the longest K),
+    decode and prefill, plus the largest M the sweep uses (4096) on a gate-shaped layer,
+    sampled against the exact products (bf16 bound 4e-3)."""
+    K, N = 22016, 8192
+    W = stack.synth_weight(N, K, 77, DEV)
+    q = sq.quantize_pack_groupwise(W)
+    rows = np.sort(np.random.default_rng(5).choice(N, 16, replace=False))
+    ref = oracle.quantize_pack(W.cpu().numpy()[rows], None)
+    W_hat = oracle.dequant(ref["Wq"], ref["scales"], ref["zeros"])
+    g = torch.Generator(device=DEV).manual_seed(78)
+    for M in (1, 16, 512):
+        X = torch.randn(M, K, generator=g, device=DEV).to(torch.bfloat16)
+        Y = sq.w4a16_gemm(X, q)
+        torch.cuda.synchronize()
+        toks = np.arange(min(M, 16))
+        x_h = X[: len(toks)].float().cpu().double().numpy()
+        y_ref = x_h @ W_hat.T
+        y = Y[: len(toks)].float().cpu().double().numpy()[:, rows]
+        err = np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref)
+        assert err <= 4e-3, (M, err)
+    # M = 4096 (prefill, several token tiles) on 8192 -> 22016
+    K2, N2 = 8192, 22016
+    W2 = stack.synth_weight(N2, K2, 79, DEV)
+    q2 = sq.quantize_pack_groupwise(W2)
+    rows2 = np.sort(np.random.default_rng(6).choice(N2, 16, replace=False))
+    ref2 = oracle.quantize_pack(W2.cpu().numpy()[rows2], None)
+    W_hat2 = oracle.dequant(ref2["Wq"], ref2["scales"], ref2["zeros"])
+    X2 = torch.randn(4096, K2, generator=g, device=DEV).half()
+    Y2 = sq.w4a16_gemm(X2, q2)
+    torch.cuda.synchronize()
+    toks = np.sort(np.random.default_rng(7).choice(4096, 24, replace=False))
+    y_ref = X2.cpu().numpy()[toks].astype(np.float64) @ W_hat2.T
+    y = Y2.cpu().numpy()[np.ix_(toks, rows2)].astype(np.float64)
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= 1e-3
