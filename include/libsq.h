@@ -204,6 +204,19 @@ SQ_API sq_status sq_smooth_activations(const void* X, int x_dtype, const float* 
                                 int64_t M, int64_t K, void* Xs, void* stream);
 
 /*
+ * Model-level smoothing fusion (Fig. 5): the
+ * activation division X diag(s)^-1 is folded into the layer that produces X.  For an
+ * RMSNorm producer the gain g[K] becomes RN(g / s), which is sq_smooth_activations on
+ * g as a [1][K] matrix.  For a linear producer (down_proj's input comes from up_proj)
+ * the producer's OUTPUT rows are divided:
+ *   W_out[n][k] = RN_dtype(W[n][k] / d[n])     (fp64 quotient, one rounding)
+ * with d = the consumer's s.  W, W_out: device [N][K] in w_dtype (may alias); d: device
+ * fp32[N] (> 0).  K % 8 == 0, 16-byte aligned W/W_out.  N == 0 is a no-op.
+ */
+SQ_API sq_status sq_fold_rows(const void* W, int w_dtype, const float* d, int64_t N, int64_t K,
+                       void* W_out, void* stream);
+
+/*
  * Squared Frobenius distance of Eq. 4: *out = sum_i (A[i] - B[i])^2 over n elements of
  * two device arrays in `dtype` (fp16/bf16), accumulated in fp64 with a fixed reduction
  * order (bit-reproducible run to run).  out: device double, written.  workspace: device,

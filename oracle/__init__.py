@@ -42,6 +42,7 @@ from .sq_oracle import (  # noqa: F401
     gemm,
     quant_loss,
     smooth_activations,
+    fold_rows,
     alpha_grid,
     layer_loss,
     alpha_search,

@@ -338,6 +338,19 @@ def smooth_activations(X: np.ndarray, s: np.ndarray, x_dtype: str = "f16") -> np
     raise ValueError(x_dtype)
 
 
+def fold_rows(W: np.ndarray, d: np.ndarray, w_dtype: str = "f16") -> np.ndarray:
+    """Model-level smoothing fusion (Fig. 5): the division of the next
+    layer's input by its smoothing factors folded into the OUTPUT rows of the producing
+    linear, W'[n][k] = RN(fp64(W[n][k]) / fp64(d[n])) to w_dtype (one rounding)."""
+    q = _as_f64(W, w_dtype) / np.asarray(d, dtype=np.float32).astype(np.float64)[:, None]
+    if w_dtype == "f16":
+        with np.errstate(over="ignore"):
+            return q.astype(np.float16)
+    if w_dtype == "bf16":
+        return rn_bf16_bits(q)
+    raise ValueError(w_dtype)
+
+
 def alpha_grid() -> np.ndarray:
     """The smoothing strengths searched: 0 to 1 at an interval of 0.05 (PAPER.md:164
     "grid search with an interval of 0.05 between 0 and 1"), 21 values,

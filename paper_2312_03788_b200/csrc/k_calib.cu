@@ -1,6 +1,8 @@
-// K-calib: the two device steps the single-layer α grid search adds to
-// the hot-path kernels.
+// K-calib: the device steps the single-layer α grid search and the
+// model-level smoothing fusion (N3, Fig. 5) add to the hot-path kernels.
 //
+//  * fold_rows:  W'[n][k] = RN_dtype(W[n][k] / d[n]) -- s^-1 folded into the output rows
+//    of the producing linear; fp64 quotient, one rounding.
 //  * smooth_activations:  X̂[m][k] = RN_dtype(X[m][k] / s[k])  -- the activation side of
 //    Eq. 5, X·diag(s)^-1.  The quotient is taken in fp64 (correctly
 //    rounded) and rounded once to fp16/bf16, so the result is bit-identical to the oracle's
@@ -9,6 +11,8 @@
 //     over two fp16/bf16 outputs.  Deterministic: a fixed grid, each
 //    CTA sums a fixed strided slice in a fixed order (thread-local fp64, then a fixed
 //    shuffle/SMEM tree), and one CTA sums the per-CTA partials in index order.
+#include <algorithm>
+
 #include "sq_internal.cuh"
 
 namespace sq {
@@ -34,11 +38,11 @@ __device__ __forceinline__ uint16_t store_rn(double v) {
 // never crosses a row.
 template <bool kBF16>
 __global__ void __launch_bounds__(kCalibThreads)
-smooth_activations_kernel(const uint4* __restrict__ X, const float* __restrict__ s, uint4* __restrict__ Xs,
+smooth_activations_kernel(const uint4* X, const float* __restrict__ s, uint4* Xs,  // X, Xs may alias
                           int64_t nvec, int64_t K) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 in = __ldg(X + v);
+    const uint4 in = X[v];
     const int64_t k0 = (v * 8) % K;
     const uint16_t* e = reinterpret_cast<const uint16_t*>(&in);
     uint4 out;
@@ -88,7 +92,42 @@ sq_diff_final_kernel(const double* __restrict__ partials, int n, double* __restr
   if (threadIdx.x == 0) *out = t;
 }
 
+// W_out[n][k] = RN_dtype(W[n][k] / d[n]): folding a smoothing factor s^-1 into the OUTPUT
+// rows of the linear that produces the smoothed activation (Fig. 5: for
+// down_proj, "the operation of dividing its input by the smoothing factor is fused into
+// the weights of up_proj").  fp64 quotient, one rounding (bit-identical to the oracle).
+template <bool kBF16>
+__global__ void __launch_bounds__(kCalibThreads)
+fold_rows_kernel(const uint4* W, const float* __restrict__ d, uint4* Wo,  // W, Wo may alias
+                 int64_t nvec, int64_t K) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 in = W[v];
+    const double dn = (double)__ldg(d + (v * 8) / K);
+    const uint16_t* e = reinterpret_cast<const uint16_t*>(&in);
+    uint4 out;
+    uint16_t* o = reinterpret_cast<uint16_t*>(&out);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = store_rn<kBF16>(__ddiv_rn(load_f64<kBF16>(e, i), dn));
+    Wo[v] = out;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fold_rows(const void* W, int dtype, const float* d, int64_t N, int64_t K, void* Wo,
+                             cudaStream_t st) {
+  const int64_t nvec = N * K / 8;
+  if (nvec == 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((nvec + kCalibThreads - 1) / kCalibThreads, (int64_t)num_sms() * 16);
+  if (dtype == SQ_BF16)
+    fold_rows_kernel<true><<<grid, kCalibThreads, 0, st>>>(static_cast<const uint4*>(W), d,
+                                                            static_cast<uint4*>(Wo), nvec, K);
+  else
+    fold_rows_kernel<false><<<grid, kCalibThreads, 0, st>>>(static_cast<const uint4*>(W), d,
+                                                             static_cast<uint4*>(Wo), nvec, K);
+  return cudaGetLastError();
+}
 
 int sq_diff_ctas() { return 4 * num_sms(); }
 

@@ -234,6 +234,19 @@ sq_status sq_smooth_activations(const void* X, int x_dtype, const float* s, int6
                      "sq_smooth_activations");
 }
 
+sq_status sq_fold_rows(const void* W, int w_dtype, const float* d, int64_t N, int64_t K, void* W_out,
+                       void* stream) {
+  g_last_error.clear();
+  if (N < 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_fold_rows: N=%lld K=%lld", (long long)N, (long long)K);
+  if (!valid_dtype(w_dtype)) return fail(SQ_ERR_UNSUPPORTED, "sq_fold_rows: dtype %d", w_dtype);
+  if (N == 0) return SQ_OK;
+  if (!W || !d || !W_out) return fail(SQ_ERR_NULL, "sq_fold_rows: null pointer");
+  if (K % 8 != 0 || !aligned16(W) || !aligned16(W_out))
+    return fail(SQ_ERR_ALIGN, "sq_fold_rows: K %% 8 != 0 or unaligned pointer");
+  return cuda_status(launch_fold_rows(W, w_dtype, d, N, K, W_out, static_cast<cudaStream_t>(stream)),
+                     "sq_fold_rows");
+}
+
 size_t sq_sq_diff_sum_workspace_bytes(void) { return (size_t)sq_diff_ctas() * sizeof(double); }
 
 sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, double* out, void* workspace,

@@ -65,7 +65,9 @@ cudaError_t launch_oneshot_allreduce(const void* y_local, int dtype, void* y_out
                                      void* const* peers_dev, int rank, int world, uint32_t epoch, int* err,
                                      cudaStream_t st);
 
-// calibration (k_calib.cu)
+// calibration / model-level smoothing folds (k_calib.cu)
+cudaError_t launch_fold_rows(const void* W, int dtype, const float* d, int64_t N, int64_t K, void* Wo,
+                             cudaStream_t st);
 int sq_diff_ctas();
 cudaError_t launch_smooth_activations(const void* X, int dtype, const float* s, int64_t M, int64_t K,
                                       void* Xs, cudaStream_t st);

@@ -65,6 +65,7 @@ def _load():
         "sq_w4a16_gemm_path": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]),
         "sq_smooth_activations": (i32, [vp, i32, vp, i64, i64, vp, vp]),
         "sq_sq_diff_sum_workspace_bytes": (sz, []),
+        "sq_fold_rows": (i32, [vp, i32, vp, i64, i64, vp, vp]),
         "sq_sq_diff_sum": (i32, [vp, vp, i32, i64, vp, vp, sz, vp]),
         "sq_allreduce_buffer_bytes": (sz, [i64, i32]),
         "sq_w4a16_gemm_allreduce": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp, i32, i32, i64,
@@ -88,7 +89,7 @@ EXPORTED = (
     "sq_get_option", "sq_act_absmax",
     "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
     "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
-    "sq_sq_diff_sum", "sq_allreduce_buffer_bytes", "sq_w4a16_gemm_allreduce", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
+    "sq_sq_diff_sum", "sq_fold_rows", "sq_allreduce_buffer_bytes", "sq_w4a16_gemm_allreduce", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
     "sq_ipc_get_handle", "sq_ipc_open_handle", "sq_ipc_close",
 )
 
@@ -325,4 +326,15 @@ def w4a16_gemm_allreduce(X: torch.Tensor, q: QuantizedLinear, peers_dev: torch.T
                                            _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes,
                                            _ptr(peers_dev), int(rank), int(world), int(n_max),
                                            ctypes.c_uint32(epoch & 0xFFFFFFFF), _ptr(error_flag), _stream(stream)))
+    return out
+
+
+def fold_rows(W: torch.Tensor, d: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """W_out[n][k] = RN(W[n][k] / d[n]): fold the consumer's smoothing factors into the
+    producer linear's output rows (Fig. 5); out may be W (in place)."""
+    _need_cuda(W, d)
+    N, K = W.shape
+    if out is None:
+        out = torch.empty_like(W)
+    _check(_load().sq_fold_rows(_ptr(W), _dtype_code(W), _ptr(d), N, K, _ptr(out), _stream(stream)))
     return out

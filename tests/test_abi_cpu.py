@@ -164,3 +164,12 @@ def test_gemm_allreduce_argument_errors(L):
     assert call(n_max=1028) == sq.SQ_ERR_ALIGN
     assert call(g=64) == sq.SQ_ERR_UNSUPPORTED
     assert call(M=0) == sq.SQ_OK
+
+
+def test_fold_rows_argument_errors(L):
+    f = L.sq_fold_rows
+    assert f(FAKE, 0, FAKE, -1, 128, FAKE, None) == sq.SQ_ERR_SHAPE
+    assert f(FAKE, 9, FAKE, 4, 128, FAKE, None) == sq.SQ_ERR_UNSUPPORTED
+    assert f(None, 0, FAKE, 4, 128, FAKE, None) == sq.SQ_ERR_NULL
+    assert f(FAKE, 0, FAKE, 4, 124, FAKE, None) == sq.SQ_ERR_ALIGN
+    assert f(None, 0, None, 0, 128, None, None) == sq.SQ_OK

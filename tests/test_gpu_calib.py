@@ -1,4 +1,5 @@
-"""GPU parity of the N2 calibration steps against the fp64 oracle.
+"""GPU parity of the N2 calibration steps and the N3 smoothing folds
+against the fp64 oracle.
 
   * sq_smooth_activations: BIT-EXACT with oracle.smooth_activations (fp16 and bf16).
   * sq_sq_diff_sum: fp64 sum of squared differences; equal to numpy's fp64 sum within
@@ -7,6 +8,7 @@
     GPU compares fp16-rounded outputs: the rounding noise is ~(5e-4 / 1e-2)^2 of the
     loss), and the chosen α is the oracle's or has a loss within 3 % of the oracle's
     minimum (a near-tie), tie rule included.
+  * sq_fold_rows (s^-1 folded into the producer's output rows, Fig. 5): BIT-EXACT.
 """
 
 from __future__ import annotations
@@ -94,3 +96,28 @@ def test_alpha_search_zero_loss_tie_rule():
     best, losses = calib.alpha_search(torch.zeros(X.shape, dtype=torch.float16, device=DEV),
                                       torch.from_numpy(W).to(DEV))
     assert best == 0.0 and bool((losses == 0).all())
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("N,K", [(1, 8), (256, 128), (1024, 4096)])
+def test_fold_rows_bitexact(N, K, dtype):
+    """Fig. 5 fusion: W'[n][k] = RN(W[n][k] / d[n]) bit-exact with the
+    oracle, in place too; and the RMSNorm-gain fold is sq_smooth_activations on g[1][K]."""
+    W = torch.from_numpy(synth.weights(N, K, seed=N)).to(dtype).to(DEV)
+    d = torch.from_numpy(np.random.default_rng(N).uniform(1e-2, 1e2, N).astype(np.float32)).to(DEV)
+    got = sq.fold_rows(W, d)
+    if dtype == torch.float16:
+        want = oracle.fold_rows(W.cpu().numpy(), d.cpu().numpy(), "f16").view(np.uint16)
+    else:
+        want = oracle.fold_rows(_bits(W), d.cpu().numpy(), "bf16")
+    assert np.array_equal(_bits(got), want)
+    Wc = W.clone()
+    sq.fold_rows(Wc, d, out=Wc)
+    assert torch.equal(Wc, got)
+    if N == 1:
+        g = W  # a gain vector g[K] as [1][K]: divide by the consumer's s (per column)
+        s = torch.from_numpy(np.random.default_rng(3).uniform(0.1, 10, K).astype(np.float32)).to(DEV)
+        gs = sq.smooth_activations(g, s)
+        ref = oracle.smooth_activations(g.cpu().numpy() if dtype == torch.float16 else _bits(g), s.cpu().numpy(),
+                                        "f16" if dtype == torch.float16 else "bf16")
+        assert np.array_equal(_bits(gs), ref.view(np.uint16) if dtype == torch.float16 else ref)

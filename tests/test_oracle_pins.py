@@ -458,3 +458,27 @@ def test_n2_search_under_outliers():
     x = X.astype(np.float64)
     rtn = float(((x @ W.astype(np.float64).T - x @ oracle.dequant(q["Wq"], q["scales"], q["zeros"]).T) ** 2).sum())
     assert losses.min() < rtn
+
+
+# ---------------------------------------------------------------- N3: model-level fusion
+def test_n3_fold_rows_exact_rational_and_mlp_equivalence():
+    """Fig. 5: dividing down_proj's input by s is fused into up_proj's
+    output rows, and down_proj's weights take s on their input channels.  (1) fold_rows is
+    the once-rounded exact quotient (exact-rational third implementation); (2) the fused
+    pair computes the same function: in fp64 with unrounded weights the results agree to
+    1e-12 relative, and with the stored fp16 weights within the two roundings' bound."""
+    r = np.random.default_rng(21)
+    Wup = (r.standard_normal((256, 128)) * 0.02).astype(np.float16)      # [N=256][K=128]
+    Wdn = (r.standard_normal((64, 256)) * 0.02).astype(np.float16)       # consumer, K = 256
+    s = r.uniform(0.05, 20.0, 256).astype(np.float32)
+    got = oracle.fold_rows(Wup, s)
+    for (n, k), wv in np.ndenumerate(Wup[:16]):
+        want = ex.rn_f16(Fraction(float(wv)) / Fraction(float(s[n])))
+        assert Fraction(float(got[n, k])) == want
+    x = r.standard_normal((8, 128))
+    ref = (x @ Wup.astype(np.float64).T) @ Wdn.astype(np.float64).T
+    exact = (x @ (Wup.astype(np.float64) / s.astype(np.float64)[:, None]).T) @ \
+        (Wdn.astype(np.float64) * s.astype(np.float64)[None, :]).T
+    assert np.linalg.norm(exact - ref) <= 1e-12 * np.linalg.norm(ref)
+    stored = (x @ got.astype(np.float64).T) @ oracle.fold(Wdn, s).T
+    assert np.linalg.norm(stored - ref) <= 2e-3 * np.linalg.norm(ref)
