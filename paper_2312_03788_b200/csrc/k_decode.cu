@@ -78,13 +78,18 @@ static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multi
 #ifndef SQ_DEC_SK_BN
 #define SQ_DEC_SK_BN 0  // stream-K row-block height: 0 = by shape (AUTO), 32 / 64 forced
 #endif
+#ifndef SQ_DEC_M1_CT3
+#define SQ_DEC_M1_CT3 1  // M = 1: 3 CTAs per SM for 32-64 MB layers that would stream-K
+#endif
 #ifndef SQ_DEC_XR4
 #define SQ_DEC_XR4 0  // 1: M = 2..4 stage 4 activation rows instead of 8 (measured -3..+5 %, net ~0)
 #endif
 #ifndef SQ_DEC_CTAS_M16
 #define SQ_DEC_CTAS_M16 2  // M = 9..16; 1 = one CTA per SM, 128-row blocks, 8 consumer warps (measured 2-35 % slower)
 #endif
-constexpr int kMaxCtasPerSm = SQ_DEC_CTAS > SQ_DEC_CTAS_M1 ? SQ_DEC_CTAS : SQ_DEC_CTAS_M1;
+constexpr int kMaxCtasPerSm0 = SQ_DEC_CTAS > SQ_DEC_CTAS_M1 ? SQ_DEC_CTAS : SQ_DEC_CTAS_M1;
+// workspace partial slots are sized for the most CTAs any decode launch can have
+constexpr int kMaxCtasPerSm = SQ_DEC_M1_CT3 && kMaxCtasPerSm0 < 3 ? 3 : kMaxCtasPerSm0;
 constexpr int kMaxBN = 128;     // row-block heights: 32 or 64 (2 CTAs/SM), 128 (1 CTA/SM)
 constexpr int kMinBN = 32;
 
@@ -987,6 +992,22 @@ double rowblock_utilization(int N, int bn, int slots) {
   return (double)rbs / ((double)waves * slots);
 }
 
+// The AUTO row-block decision (see launch_m): true and the row height if whole row blocks win.
+bool auto_rowblock(int N, int K, int slots, int* bn_out) {
+  const int G = K / kGroup;
+  const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
+      (double)((N + 63) / 64) * ((G + GPS - 1) / GPS));
+  for (int cand : {32, 64}) {
+    const int rbs = (N + cand - 1) / cand;
+    const double rb_bytes = (double)cand * K / 2;
+    if (rbs <= slots && rb_bytes - sk_bytes_per_cta <= 48.0 * 1024 && rb_bytes <= 192.0 * 1024) {
+      *bn_out = cand;
+      return true;
+    }
+  }
+  return false;
+}
+
 template <int MT, bool kBF16, int XR, int CT>
 cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, const ArParams& ar, cudaStream_t st,
@@ -1006,9 +1027,6 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // 34B o_proj 8192 x 8192 (+15 KB, 128 KB), 7B qkv 4096 x 12288 (+46 KB, 128 KB) and 7B
   // o_proj 4096 x 4096 (+36 KB, 64 KB) take row blocks; 34B qkv (+114 KB), 34B down_proj
   // (+47 KB but 352 KB per CTA) and the rest stay stream-K.
-  const int G = K / kGroup;
-  const double sk_bytes_per_cta = (double)N * K / 2 / std::min<double>((double)slots,
-      (double)((N + 63) / 64) * ((G + GPS - 1) / GPS));
   bool dp = sched == SQ_SCHED_ROWBLOCK;
   // stream-K row-block height: 32 rows for M = 9..16 on layers below 48 MB of codes (half
   // the cut row blocks' fixup work; measured -8..-13 % on the 7B shapes, +2 % on 34B qkv),
@@ -1017,14 +1035,10 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   if (sched == SQ_SCHED_ROWBLOCK) {
     bn = rowblock_utilization(N, 64, slots) >= rowblock_utilization(N, 32, slots) ? 64 : 32;
   } else if (sched == SQ_SCHED_AUTO) {
-    for (int cand : {32, 64}) {
-      const int rbs = (N + cand - 1) / cand;
-      const double rb_bytes = (double)cand * K / 2;
-      if (rbs <= slots && rb_bytes - sk_bytes_per_cta <= 48.0 * 1024 && rb_bytes <= 192.0 * 1024) {
-        dp = true;
-        bn = cand;
-        break;
-      }
+    int rbn = 64;
+    if (auto_rowblock(N, K, slots, &rbn)) {
+      dp = true;
+      bn = rbn;
     }
   }
   if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
@@ -1049,9 +1063,19 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
   constexpr int C2 = SQ_DEC_CTAS, C1 = SQ_DEC_CTAS_M1;
-  if (M == 1)  // batch-1 decode: stage one activation row, smaller stages, more CTAs per SM
+  if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
+    // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
+    // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
+    // measured -12 % on 7B gate|up, -2 % on 34B qkv (profiles/decode_m1_ct3_ab_r01.jsonl)
+    const double codes = (double)N * K / 2;
+    int rbn = 64;
+    if (SQ_DEC_M1_CT3 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO && codes >= 32.0 * 1024 * 1024 &&
+        codes <= 64.0 * 1024 * 1024 && !auto_rowblock(N, K, num_sms() * C1, &rbn))
+      return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
+                  : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
     return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
                 : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+  }
 #if SQ_DEC_XR4
   if (M <= 4)  // stage four activation rows
     return bf16 ? launch_m<1, true, 4, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
