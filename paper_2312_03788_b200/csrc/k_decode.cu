@@ -81,6 +81,9 @@ static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multi
 #ifndef SQ_DEC_M1_CT3
 #define SQ_DEC_M1_CT3 1  // M = 1: 3 CTAs per SM for 32-64 MB layers that would stream-K
 #endif
+#ifndef SQ_DEC_EVICT_FIRST
+#define SQ_DEC_EVICT_FIRST 1  // codes TMA with an L2 evict-first policy
+#endif
 #ifndef SQ_DEC_XR4
 #define SQ_DEC_XR4 0  // 1: M = 2..4 stage 4 activation rows instead of 8 (measured -3..+5 %, net ~0)
 #endif
@@ -178,6 +181,19 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, uint3
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+// weights are streamed exactly once: load them with an L2 evict-first policy so they do
+// not push the activations / partials (re-read across CTAs and kernels) out of L2
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_3d_hint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy) : "memory");
 }
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
   asm volatile(
@@ -435,9 +451,13 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       prefetch_tmap(&tm_x);
       prefetch_tmap(&tm_s);
       prefetch_tmap(&tm_z);
+      const uint64_t wpol = SQ_DEC_EVICT_FIRST ? l2_evict_first_policy() : 0;
       auto load_weights = [&](uint32_t st, uint32_t fb, int u) {
         const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
-        tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+        if (SQ_DEC_EVICT_FIRST)
+          tma_3d_hint(st, &tm_w, fb, 0, rb * BN, g0, wpol);
+        else
+          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
         tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
         tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
       };
