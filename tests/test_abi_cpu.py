@@ -173,3 +173,24 @@ def test_fold_rows_argument_errors(L):
     assert f(None, 0, FAKE, 4, 128, FAKE, None) == sq.SQ_ERR_NULL
     assert f(FAKE, 0, FAKE, 4, 124, FAKE, None) == sq.SQ_ERR_ALIGN
     assert f(None, 0, None, 0, 128, None, None) == sq.SQ_OK
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/libsq.h is a plain C ABI: it compiles as pedantic C99 (no C++ or torch
+    types) and a C program links against libsq.so and calls into it (no GPU needed)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "abi.c"
+    src.write_text('#include "libsq.h"\nint main(void) { return sq_version() > 0 && '
+                   'sq_allreduce_buffer_bytes(8, 2) > 0 ? 0 : 1; }\n')
+    libdir = os.path.dirname(sq.LIB_PATH)
+    exe = tmp_path / "abi"
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                        os.path.join(ROOT, "include"), str(src), "-L", libdir, "-lsq",
+                        f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(exe)]).returncode == 0
