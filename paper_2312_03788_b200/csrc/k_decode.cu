@@ -521,14 +521,14 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     const int par = epoch & 1;
     auto emit = [&](int rb, const float (&val)[E]) {  // final values of row block rb
       const int n0 = rb * BN;
-      if (!kAR) {
+      if constexpr (!kAR) {
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
           if (t < M && n0 + row < N) Y[(size_t)t * N + n0 + row] = to_out(val[i]);
         }
         return;
-      }
+      } else {
       for (int p = 0; p < ar.world; ++p) {
         uint16_t* dst = ar_slots(ar.peers[p], ar.world, par, ar.rank, ar.n_max);
 #pragma unroll
@@ -550,6 +550,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       }
       ++n_fin;
       __syncwarp();
+      }
     };
     for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
       const int rb = sc.u / wk.upb;

@@ -17,9 +17,9 @@
 //  * r = hi - lo in fp64 (exact for fp16 inputs), Δ = RZ16(r/15) via fp64 division
 //    then RZ->fp32->RZ->fp16 (RZ∘RZ = RZ).
 //  * codes (fp16 path): t = v * RN(1/Δ) has |error| <= 2^-19 for |t| < 16 while a
-//    non-tie v/Δ is >= 2^-12 from any half-integer (fp16 v, Δ), so roundf(t) is the
-//    RHA of v/Δ except at exact ties, which are detected exactly with one FMA
-//    (v - (k+1/2)Δ is computed exactly) and rounded away from zero.
+//    non-tie v/Δ is >= 2^-12 from any half-integer (fp16 v, Δ), so trunc(t ± 1/2) is the
+//    RHA of v/Δ except at an exact tie that t missed, which one branch-free FMA detects
+//    exactly (v - (c ± 1/2)Δ is computed exactly) and moves away from zero.
 //  * codes (bf16 path): the gap can be as small as 2^-20, so v/Δ uses fp64 division.
 #include <algorithm>
 
@@ -80,16 +80,17 @@ __device__ __forceinline__ uint16_t fold1(uint16_t wbits, float s) {
   return Fmt<kBF16>::from_f_rn(p);
 }
 
-// RHA(v / d) for fp16 v, d (see header comment), as float.
+// RHA(v / d) for fp16 v, d (see header comment), as float, branch-free.  t = v * RN(1/d)
+// is within 2^-19 of x = v/d (|x| < 16) while a non-tie x is >= 2^-12 from every k + 1/2,
+// so c = trunc(t + copysign(1/2, t)) is RHA(x) unless x is an exact tie that t missed by
+// rounding toward zero; then v - (c + copysign(1/2, t)) d is exactly 0 (one FMA, the
+// product is exact) and c moves one step away from zero.  A nonzero exact difference
+// never rounds to 0, so non-ties are never moved.
 __device__ __forceinline__ float rha_div_f16(float v, float d, float inv) {
   const float t = v * inv;
-  float r = roundf(t);
-  const float tr = truncf(t);
-  const float h = tr + copysignf(0.5f, t);
-  if (fabsf(t - h) < 0x1p-16f) {
-    if (__fmaf_rn(-h, d, v) == 0.0f) r = tr + copysignf(1.0f, t);
-  }
-  return r;
+  const float h = copysignf(0.5f, t);
+  const float c = truncf(t + h);
+  return __fmaf_rn(-(c + h), d, v) == 0.0f ? c + 2.0f * h : c;
 }
 
 template <bool kBF16>
