@@ -184,7 +184,9 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
           c = rha_div_f16(v, d, inv);
         }
         c = fminf(fmaxf(c + z, 0.0f), 15.0f);
-        packed[i >> 3] |= ((uint32_t)c) << (4 * (i & 7));
+        // integral c in [0, 15]: c + 2^23 is exact and its low mantissa bits are c (no
+        // float->int conversion instruction)
+        packed[i >> 3] |= (__float_as_uint(c + 8388608.0f) & 0xFu) << (4 * (i & 7));
       }
     }
     if (row_ok) {
