@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--layers", type=int, default=48)
     ap.add_argument("--decode-m", type=str, default="1,4,16")
+    ap.add_argument("--c4-m", type=str, default="32,64",
+                    help="extra decode batches above M_dec reported in c4_batches (not in the headline)")
     ap.add_argument("--prefill-m", type=int, default=2048)
     ap.add_argument("--prefill-layers", type=int, default=4)
     ap.add_argument("--skip-prefill", action="store_true")
@@ -172,6 +174,58 @@ def oracle_decode_sample(ms, rows=1024, K=8192, seed=1234):
     return total_b, total_t, desc
 
 
+def oracle_quantize_and_c1():
+    """SURVEY.md §8(d) "Oracle timing": the fp64 oracle's quantize (a1-a4: Eq. 6 + Eq. 5
+    fold + Eq. 1) on a bounded sample of a 34B layer, and the whole C1 pipeline
+    (BASELINE.json configs[0]) on ONE host thread."""
+    import numpy as np
+
+    import oracle
+    from paper_2312_03788_b200 import synth
+
+    out = {}
+    rows, K = 2048, 8192
+    W = synth.weights(rows, K, seed=21)
+    am = oracle.act_absmax(synth.activations(1024, K, seed=22).astype(np.float16))
+    t0 = time.perf_counter()
+    s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
+    oracle.quantize_pack(W, s, 128)
+    tq = time.perf_counter() - t0
+    qbytes = 2 * rows * K * 2 + 4 * K + rows * K // 2 + 4 * rows * (K // 128)
+    out["quantize"] = {"value": qbytes / tq / 1e9, "unit": "GB/s", "seconds": tq,
+                       "sample": f"oracle smooth_scales + quantize_pack on {rows} rows of a K={K} layer "
+                                 "(same algorithmic bytes as the GPU quantize line)"}
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        threadpool_limits = None
+    N1 = K1 = 512
+    W1 = synth.weights(N1, K1, seed=0)
+    Xc = synth.activations(164 * 16, K1, seed=1).astype(np.float16)
+    X1 = synth.activations(1, K1, seed=2, outlier_seed=1).astype(np.float16)
+
+    def c1():
+        a_ = oracle.act_absmax(Xc)
+        s_ = oracle.smooth_scales(oracle.weight_absmax(W1), a_, 0.5)
+        q_ = oracle.quantize_pack(W1, s_, 128)
+        xh = oracle.smooth_activations(X1, s_)
+        return oracle.gemm(xh, q_["Wq"], q_["scales"], q_["zeros"])
+
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            c1()
+            t1 = time.perf_counter() - t0
+    else:
+        t0 = time.perf_counter()
+        c1()
+        t1 = time.perf_counter() - t0
+    out["c1_single_thread"] = {"seconds": t1, "threads": 1 if threadpool_limits is not None else blas_threads(),
+                               "what": "configs[0] pipeline: act_absmax (2624 calib rows) -> Eq. 6 -> Eq. 5+1 "
+                                       "quantize -> X/s -> W4A16 GEMM, M=1, K=N=512, fp64 oracle"}
+    return out
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -205,6 +259,97 @@ def run_reference(a, rank):
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def tp_reduction_error(st, dev, rank, world, pg, M=4, rows=48):
+    """Max relative Frobenius error (fp16 and bf16 activations) of the row-parallel layers'
+    all-reduced output vs the fp64 oracle of the whole layer: each rank's shard of the codes
+    / scales / zeros of `rows` sampled output channels and its activation slice are gathered
+    to every rank; the oracle sums Σ_r X_r Ŵ_rᵀ exactly."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2312_03788_b200 import sq, stack
+
+    res = {}
+    for dt, name in ((torch.float16, "f16"), (torch.bfloat16, "bf16")):
+        worst = 0.0
+        for si, sh in enumerate(st.shards):
+            if not sh.allreduce:
+                continue
+            lin = st.layers[0][si]
+            g = torch.Generator(device=dev).manual_seed(77 + si)
+            N = sh.N
+            ridx = torch.from_numpy(np.sort(np.random.default_rng(si).choice(N, rows, replace=False))).to(dev)
+            # full activations, identical on every rank, and this rank's K slice
+            Kfull = int(sum_k(sh.K, world, pg, dev))
+            k0 = int(exclusive_k(sh.K, world, rank, pg, dev))
+            X = torch.randn(M, Kfull, generator=g, device=dev).to(dt)
+            x = X[:, k0:k0 + sh.K].contiguous()
+            y = torch.empty(M, N, dtype=dt, device=dev)
+            buf = stack.PassBuffers(M, {sh.name: x}, {sh.name: y})
+            one = stack.LinearStack(st.model, rank, world, layers=[[lin]], group=st.group, peer_ar=st.peer_ar)
+            stack.run_pass(one, buf)
+            torch.cuda.synchronize()
+            # gather the sampled rows of every rank's shard (pad K to the max over ranks)
+            kmax = int(max_k(sh.K, world, pg, dev))
+            Gm = kmax // 128
+            wq = torch.zeros(rows, kmax // 2, dtype=torch.uint8, device=dev)
+            wq[:, :sh.K // 2] = lin.q.Wq[ridx]
+            sc = torch.zeros(Gm, rows, dtype=torch.int16, device=dev)
+            sc[:sh.K // 128] = lin.q.scales[:, ridx]
+            zr = torch.zeros(Gm, rows, dtype=torch.int16, device=dev)
+            zr[:sh.K // 128] = lin.q.zeros[:, ridx]
+            ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+            dist.all_gather(ks, torch.tensor([sh.K], device=dev), group=pg)
+            parts = []
+            for t in (wq, sc, zr):
+                lst = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(lst, t, group=pg)
+                parts.append([v.cpu().numpy() for v in lst])
+            xs = X.float().cpu().double().numpy()
+            y_ref = np.zeros((M, rows))
+            off = 0
+            for r in range(world):
+                Kr = int(ks[r].item())
+                W_hat = oracle.dequant(parts[0][r][:, :Kr // 2], parts[1][r][:Kr // 128].view(np.uint16),
+                                       parts[2][r][:Kr // 128].view(np.uint16))
+                y_ref += xs[:, off:off + Kr] @ W_hat.T
+                off += Kr
+            yg = y[:, ridx].float().cpu().double().numpy()
+            worst = max(worst, float(np.linalg.norm(yg - y_ref) / np.linalg.norm(y_ref)))
+        res[name] = worst
+    res.update({"P": world, "M": M, "rows_sampled": rows, "layers": "row-parallel (o_proj, down_proj) of layer 0",
+                "bound": {"f16": 1e-3, "bf16": 4e-3}})
+    return res
+
+
+def _reduce_scalar(v, op, pg, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=op, group=pg)
+    return float(t.item())
+
+
+def sum_k(k, world, pg, dev):
+    import torch.distributed as dist
+    return _reduce_scalar(k, dist.ReduceOp.SUM, pg, dev)
+
+
+def max_k(k, world, pg, dev):
+    import torch.distributed as dist
+    return _reduce_scalar(k, dist.ReduceOp.MAX, pg, dev)
+
+
+def exclusive_k(k, world, rank, pg, dev):
+    import torch
+    import torch.distributed as dist
+    lst = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(lst, torch.tensor([float(k)], dtype=torch.float64, device=dev), group=pg)
+    return sum(float(lst[r].item()) for r in range(rank))
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -256,6 +401,35 @@ def main():
         dist.all_reduce(t)
         return float(t.item())
 
+    def chain_time(stk, si, b, reps, graph_ok=True):
+        """Seconds per launch of linear `si` chained over all of stk's layers (one CUDA graph of
+        len(stk.layers) dependent launches on the stack's resident weights)."""
+        sh = stk.shards[si]
+
+        def chain():
+            for row in stk.layers:
+                sq.w4a16_gemm(b.x[sh.name], row[si].q, out=b.y[sh.name])
+        chain()
+        torch.cuda.synchronize()
+        run = chain
+        gch = None
+        if graph_ok:
+            gch = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gch):
+                chain()
+            run = gch.replay
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        del gch
+        return e0.elapsed_time(e1) * 1e-3 / (reps * len(stk.layers))
+
     # ---------------- decode stack (the headline)
     st = stack.build_stack(model, a.layers, rank, world, dev, group=pg)
     torch.cuda.synchronize()
@@ -266,10 +440,17 @@ def main():
         ar_impl = "nccl"
         if a.ar == "peer":
             ar_impl = stack.attach_peer_allreduce(st, max(ms) * model.hidden, dev)
-    # inference: the quantized weights are resident and never written while the GEMMs
-    # run, so the decode kernel may stream them ahead of the previous kernel (PDL)
-    sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
-    launch_opts = {"pdl": sq.get_option(sq.SQ_OPT_PDL), "weights_static": sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC)}
+    # inference: the quantized weights are resident and never written while the GEMMs run
+    # (build_stack marks every handle static, so each GEMM passes SQ_GEMM_WEIGHTS_STATIC and
+    # the decode kernel may stream weights ahead of the previous kernel under PDL)
+    launch_opts = {"pdl": sq.get_option(sq.SQ_OPT_PDL),
+                   "weights_static": all(l.q.static for row in st.layers for l in row)}
+    # ---------------- error of the tensor-parallel reduction at this P, per
+    # dtype -- the row-parallel layers' reduced Y (through the path the stack uses) against the
+    # fp64 oracle of the unsharded layer (all ranks' shards) on sampled output rows
+    tp_error = None
+    if world > 1:
+        tp_error = tp_reduction_error(st, dev, rank, world, pg)
     bufs = [stack.make_buffers(st, M, dev) for M in ms]
     if world > 1:
         t = torch.ones(1, device=dev)
@@ -366,12 +547,57 @@ def main():
                            "frac_hbm": bm / tm / 1e9 / hbm_peak / world}
         del g2
 
+    # ---------------- BASELINE.json configs[3] decode batches above M_dec (32, 64): the
+    # same stack pass at those M (the prefill kernel serves them), reported next to per_m
+    c4 = {}
+    for M in [int(x) for x in a.c4_m.split(",") if x]:
+        b4 = stack.make_buffers(st, M, dev)
+        ws4 = torch.zeros(max(16, max(sq.w4a16_gemm_workspace_bytes(M, sh.N, sh.K) for sh in st.shards)),
+                          dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            stack.run_pass(st, b4, workspace=ws4)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(2, a.steps // 6)
+        e0.record()
+        for _ in range(reps):
+            stack.run_pass(st, b4, workspace=ws4)
+        e1.record()
+        torch.cuda.synchronize()
+        tm = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / reps)
+        bm = sum_over_ranks(float(stack.pass_bytes(st, M)))
+        fm = sum_over_ranks(float(stack.pass_flops(st, M)))
+        # roofline at this M: min(HBM, tensor) bound of the algorithmic bytes and flops
+        t_roof = max(bm / world / (hbm_peak * 1e9), fm / world / (peaks.get("bf16_tflops", 1.0) * 1e12))
+        c4[str(M)] = {"ms_per_pass": tm * 1e3, "GB/s": bm / tm / 1e9, "TFLOP/s": fm / tm / 1e12,
+                      "frac_roofline": t_roof / tm, "path": "prefill kernel (M > 16)"}
+        del b4, ws4
+
+    # ---------------- SURVEY.md §8(d) gates, per shape: each 34B linear timed as a chain of
+    # its 48 layers (48 dependent launches of one shape, the stack's own resident weights,
+    # 48 x the shape's bytes >> L2) in one CUDA graph; decode at every M of the step
+    gates = {"decode": {}, "prefill": {}}
+    if world == 1:
+        for si, sh in enumerate(st.shards):
+            rows = {}
+            for b in bufs:
+                t_l = chain_time(st, si, b, max(3, a.steps // 3), not a.no_graph)
+                bl = tp.decode_bytes(b.M, sh.K, sh.N)
+                rows[str(b.M)] = {"us_per_launch": t_l * 1e6, "GB/s": bl / t_l / 1e9,
+                                  "frac": bl / t_l / 1e9 / hbm_peak, "bytes": bl}
+            gates["decode"][f"{sh.name} {sh.K}x{sh.N}"] = rows
+        fr = [(r["frac"], r["bytes"]) for d in gates["decode"].values() for r in d.values()]
+        gates["decode_summary"] = {"target": 0.75, "min_frac": min(f for f, _ in fr),
+                                   "byte_weighted_mean_frac": sum(f * b_ for f, b_ in fr) / sum(b_ for _, b_ in fr),
+                                   "how": "per 34B linear x M in the step: 48-launch CUDA-graph chain of the "
+                                          "shape's layers, algorithmic bytes / event time per launch"}
+
     # ---------------- BASELINE.json configs[1]: Code Llama-7B decode shapes on 1 GPU
     cfg7 = None
     if world == 1 and not a.skip_7b:
         m7 = tp.CODELLAMA_7B
         st7 = stack.build_stack(m7, m7.layers, 0, 1, dev)
-        per7, tot_b, tot_t = {}, 0.0, 0.0
+        per7, shapes7, tot_b, tot_t = {}, {}, 0.0, 0.0
         for M in ms:
             b7 = stack.make_buffers(st7, M, dev)
             g7 = None
@@ -400,11 +626,18 @@ def main():
             per7[str(M)] = {"ms_per_pass": tm * 1e3, "GB/s": bm / tm / 1e9, "frac_hbm": bm / tm / 1e9 / hbm_peak}
             tot_b += bm
             tot_t += tm
-            del g7, b7
+            del g7
+            for si, sh in enumerate(st7.shards):
+                t_l = chain_time(st7, si, b7, max(3, a.steps // 3), not a.no_graph)
+                bl = tp.decode_bytes(M, sh.K, sh.N)
+                shapes7.setdefault(f"{sh.name} {sh.K}x{sh.N}", {})[str(M)] = {
+                    "us_per_launch": t_l * 1e6, "GB/s": bl / t_l / 1e9, "frac": bl / t_l / 1e9 / hbm_peak}
+            del b7
         cfg7 = {"workload": "codellama-7b-w4a16-linear-stack-decode (BASELINE.json configs[1])",
                 "layers": m7.layers, "linears": [s_.name for s_ in st7.shards],
                 "shapes_KxN": [[s_.K, s_.N] for s_ in st7.shards], "value": tot_b / tot_t / 1e9,
-                "unit": "GB/s", "frac_hbm": tot_b / tot_t / 1e9 / hbm_peak, "per_m": per7}
+                "unit": "GB/s", "frac_hbm": tot_b / tot_t / 1e9 / hbm_peak, "per_m": per7,
+                "per_shape": shapes7}
         del st7
         torch.cuda.empty_cache()
 
@@ -468,6 +701,7 @@ def main():
         flops_all = sum_over_ranks(float(flops_rank))
         tf = flops_all / tpre / 1e12
         tc_peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])  # fp16 dense == bf16 dense
+        tc_sus = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"])
         n_l = len(pst.layers) * len(pst.shards)
         ach = flops_rank / tp_rank / 1e12
         prefill = {"value": tf, "unit": "TFLOP/s", "M": M, "layers": len(pst.layers),
@@ -478,12 +712,36 @@ def main():
                                 "kernel": "sq::prefill_kernel (TMA + tcgen05.mma, A in TMEM)",
                                 "peak_source": f"{peaks_src} bf16_tflops (fp16 dense = bf16 dense)",
                                 "flops_per_launch": flops_rank / n_l}}
+        if world == 1:  # §8(d) prefill gate per 34B shape (each over the pass's layers)
+            for si, sh in enumerate(pst.shards):
+                def pchain(si=si, sh=sh):
+                    for row in pst.layers:
+                        sq.w4a16_gemm(pb.x[sh.name], row[si].q, out=pb.y[sh.name], workspace=ws)
+                pchain()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    pchain()
+                e1.record()
+                torch.cuda.synchronize()
+                t_l = e0.elapsed_time(e1) * 1e-3 / (reps * len(pst.layers))
+                fl = tp.gemm_flops(M, sh.K, sh.N)
+                gates["prefill"][f"{sh.name} {sh.K}x{sh.N}"] = {
+                    "us_per_launch": t_l * 1e6, "TFLOP/s": fl / t_l / 1e12, "frac": fl / t_l / 1e12 / tc_sus,
+                    "frac_burst_peak": fl / t_l / 1e12 / tc_peak, "flops": fl}
+            pr = list(gates["prefill"].values())
+            gates["prefill_summary"] = {
+                "target": 0.60, "M": M, "min_frac": min(r["frac"] for r in pr),
+                "flop_weighted_mean_frac": sum(r["frac"] * r["flops"] for r in pr) / sum(r["flops"] for r in pr),
+                "peak": f"{tc_sus} TF/s = MEASURED_PEAKS bf16_tflops_sustained (each shape: {reps} x "
+                        f"{len(pst.layers)} back-to-back launches of ~0.3-1.3 ms under the board's power cap); "
+                        f"frac_burst_peak against {tc_peak}"}
         del pb, ws
         torch.cuda.empty_cache()
 
     # ---------------- load-time smoothing + quantization (a1-a4)
     quant = None
-    sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 0)  # quantize writes the weights GEMMs read
     if not a.skip_quant:
         Ws, ams = [], []
         for si, sh in enumerate(st.shards):
@@ -558,6 +816,7 @@ def main():
             t_tot += tt
         cpu = {"value": b_tot / t_tot / 1e9, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
                "sample": desc + f"; repeated for {t_tot:.1f} s"}
+        cpu.update(oracle_quantize_and_c1())
 
     if rank == 0:
         line = {
@@ -575,12 +834,15 @@ def main():
             "clocks": clocks,
             "roofline": roofline,
             "per_m": per_m,
+            "c4_batches": c4,
+            "gates": gates,
             "prefill": prefill,
             "quantize": quant,
             "calibration": calib_res,
             "codellama_7b_decode": cfg7,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "tp_error": tp_error,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -70,25 +70,28 @@ enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
  *    launch, so a kernel's prologue overlaps the previous kernel's tail; every
  *    read of X and every global write still waits for the previous kernel
  *    (griddepcontrol.wait), so results are unchanged.
- *  SQ_OPT_WEIGHTS_STATIC (default 0): the caller promises that Wq/scales/zeros
- *    are not written by the kernels that immediately precede a GEMM on its
- *    stream (true for inference with resident weights).  The decode kernel then
- *    streams its first weight stages BEFORE waiting on the previous kernel.
  *  SQ_OPT_DECODE_SCHEDULE (default SQ_SCHED_AUTO): how the decode kernel splits
  *    the weight matrix over its persistent CTAs.  SQ_SCHED_STREAMK: equal
  *    contiguous ranges of (row block x 4 groups) units, row blocks cut between
  *    CTAs finished by a deterministic fixup through the workspace.
  *    SQ_SCHED_ROWBLOCK: whole row blocks (32 or 64 rows) per CTA, no fixup.
- *    AUTO takes ROWBLOCK when its wave quantization keeps >= 85 % of the CTAs
- *    busy, STREAMK otherwise.  Results agree to fp32 rounding either way.
- *  SQ_OPT_DECODE_KERNEL (default SQ_DECK_MMA_SYNC): the decode-path kernel.
- *    SQ_DECK_MMA_SYNC: warp-level mma.sync on register fragments (k_decode.cu).
- *    SQ_DECK_TCGEN05: 5th-gen tensor cores, weights as the 128-row A operand in TMEM,
- *    one TMEM accumulator per group (k_decode_tc.cu).  Same numerics (exact q - Z
- *    operands, Δ applied per group in fp32). */
-enum { SQ_OPT_PDL = 1, SQ_OPT_WEIGHTS_STATIC = 2, SQ_OPT_DECODE_SCHEDULE = 3, SQ_OPT_DECODE_KERNEL = 4 };
+ *    AUTO picks per shape.  Results agree to fp32 rounding either way.
+ *  SQ_OPT_DECODE_GRID_LIMIT (default 0 = none): at most this many CTAs per decode
+ *    launch.  For tests that run several simulated tensor-parallel ranks of
+ *    sq_w4a16_gemm_allreduce as concurrent kernels on ONE GPU (their grids must be
+ *    co-resident); results do not depend on it.
+ * Option 2 (a process-wide "weights static" switch in version 1) is now the per-call
+ * flag SQ_GEMM_WEIGHTS_STATIC; sq_set_option(2, ...) returns SQ_ERR_UNSUPPORTED. */
+enum { SQ_OPT_PDL = 1, SQ_OPT_DECODE_SCHEDULE = 3, SQ_OPT_DECODE_GRID_LIMIT = 5 };
 enum { SQ_SCHED_AUTO = 0, SQ_SCHED_STREAMK = 1, SQ_SCHED_ROWBLOCK = 2 };
-enum { SQ_DECK_MMA_SYNC = 0, SQ_DECK_TCGEN05 = 1 };
+/* Per-call GEMM flags (sq_w4a16_gemm_ex, sq_w4a16_gemm_allreduce):
+ *  SQ_GEMM_WEIGHTS_STATIC: the caller promises that Wq/scales/zeros of THIS call are
+ *    not written by the kernels that precede it on its stream (true for inference with
+ *    resident weights; false right after sq_quantize_pack_groupwise wrote them).  With
+ *    PDL the kernel then streams its first weight stages BEFORE waiting on the previous
+ *    kernel; X and every global write still wait.  Without the flag the weights are
+ *    read only after the previous kernel has completed. */
+enum { SQ_GEMM_WEIGHTS_STATIC = 1u };
 
 /* Library version (major*10000 + minor*100 + patch). */
 SQ_API int sq_version(void);
@@ -130,6 +133,18 @@ SQ_API sq_status sq_smooth_scales(const void* W, int w_dtype, int64_t N, int64_t
                            float* s_out, void* stream);
 
 /*
+ * Eq. 6 from precomputed maxima: s[k] = RN_fp32(max(act_max[k],eps)^alpha /
+ * max(w_max[k],eps)^(1-alpha)), the same evaluation as sq_smooth_scales.  For weights
+ * sharded over ranks (tensor parallel), w_max is the column abs-max of the FULL weight:
+ * each rank takes sq_act_absmax of its shard (a [N_r][K] matrix's column maxima) and the
+ * ranks all-reduce it with MAX before this call, so every rank folds the same s.
+ * w_max, act_max: fp32[K] device, read; s_out: fp32[K] device, written (may alias w_max,
+ * must not alias act_max).  16-byte aligned pointers.
+ */
+SQ_API sq_status sq_smooth_scales_wmax(const float* w_max, const float* act_max, int64_t K,
+                                double alpha, double eps, float* s_out, void* stream);
+
+/*
  * Eq. 5 + Eq. 1 (load-time quantization).  For every output
  * channel n and group gi of `group` consecutive input channels:
  *   W'[n][k] = RN(W[n][k] * s[k]) to w_dtype, one rounding    (s == NULL: RTN, s = 1)
@@ -155,11 +170,16 @@ SQ_API sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const fl
  * Bytes of caller-allocated device workspace sq_w4a16_gemm needs for this shape
  * (the decode path's stream-K fixup: fp32 partial tiles, then per-row-block
  * counters).  The workspace must be 16-byte aligned and zero-filled once before
- * its first use; every call leaves the counters zero again, so one workspace can
- * serve any sequence of shapes on one stream.  Calls that may run concurrently
- * (different streams) need different workspaces.
+ * its first use (sq_workspace_reset); every completed call leaves the counters zero
+ * again, so one workspace can serve any sequence of shapes on one stream.  Calls
+ * that may run concurrently (different streams) need different workspaces.  After a
+ * launch that did not complete (an error, a killed context) reset the workspace before
+ * reusing it: stale counters would mis-identify the last stream-K contributor.
  */
 SQ_API size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group);
+/* Zero-fill a GEMM workspace (or an all-reduce symmetric buffer) on `stream`
+ * (cudaMemsetAsync).  workspace_bytes == 0 is a no-op. */
+SQ_API sq_status sq_workspace_reset(void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Eq. 3, W4A16 linear layer:
@@ -177,8 +197,15 @@ SQ_API sq_status sq_w4a16_gemm(const void* X, int x_dtype,
                         void* Y, int64_t M, int64_t N, int64_t K, int group,
                         void* workspace, size_t workspace_bytes, void* stream);
 
-/* Same as sq_w4a16_gemm with an explicit path (SQ_PATH_*), for the M sweep and
- * the parity tests.  SQ_PATH_DECODE requires M <= 16. */
+/* Same as sq_w4a16_gemm with an explicit path (SQ_PATH_*: AUTO, DECODE for M <= 16,
+ * PREFILL) and per-call flags (SQ_GEMM_WEIGHTS_STATIC or 0; other bits ->
+ * SQ_ERR_UNSUPPORTED).  sq_w4a16_gemm == sq_w4a16_gemm_ex(..., SQ_PATH_AUTO, 0, stream). */
+SQ_API sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype,
+                           const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                           void* Y, int64_t M, int64_t N, int64_t K, int group,
+                           void* workspace, size_t workspace_bytes, int path, unsigned flags,
+                           void* stream);
+/* sq_w4a16_gemm_ex with flags = 0 (kept for the M sweep and the parity tests). */
 SQ_API sq_status sq_w4a16_gemm_path(const void* X, int x_dtype,
                              const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                              void* Y, int64_t M, int64_t N, int64_t K, int group,
@@ -247,8 +274,10 @@ SQ_API sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t
  * mode per buffer.
  * n <= n_max elements of dtype (fp16/bf16) in y_local and y_out (may alias).  error_flag:
  * device int, set to 1 if a peer did not arrive within the bounded wait (~seconds); the
- * kernel then leaves y_out partially written instead of hanging.  Stream-ordered; every
- * rank must make the matching call (a collective).
+ * kernel then leaves y_out partially written instead of hanging (the buffer header stays
+ * consistent; to restart a broken collective, zero every rank's buffer with
+ * sq_workspace_reset and restart the epochs).  Stream-ordered; every rank must make the
+ * matching call (a collective).
  */
 SQ_API size_t sq_allreduce_buffer_bytes(int64_t n_max, int world);
 SQ_API sq_status sq_allreduce_oneshot(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,
@@ -265,15 +294,19 @@ SQ_API sq_status sq_allreduce_oneshot(const void* y_local, int dtype, void* y_ou
  * For M > sq_decode_max_m() (prefill) this is sq_w4a16_gemm followed by
  * sq_allreduce_oneshot on Y.  Arguments: those of sq_w4a16_gemm (X is this rank's input
  * shard [M][K_r], Wq/scales/zeros its row-parallel weight shard) plus those of
- * sq_allreduce_oneshot with n_max >= M*N.  A buffer serves either this call or
- * sq_allreduce_oneshot calls, in the same epoch mode, in one stream order on every rank.
+ * sq_allreduce_oneshot with n_max >= M*N, and the per-call flags of sq_w4a16_gemm_ex.
+ * fp16 partials are exchanged in fp16, bf16 partials in fp32; the sum
+ * is always taken in fp32.  Every rank must cut N into the same row blocks, so the decode
+ * schedule here depends on N and M only, never on the rank's K.  A buffer serves either
+ * this call or sq_allreduce_oneshot calls, in the same epoch mode, in one stream order on
+ * every rank.
  */
 SQ_API sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype,
                                   const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                                   void* Y, int64_t M, int64_t N, int64_t K, int group,
                                   void* workspace, size_t workspace_bytes,
                                   void* const* peer_bufs, int rank, int world, int64_t n_max,
-                                  uint32_t epoch, int* error_flag, void* stream);
+                                  uint32_t epoch, int* error_flag, unsigned flags, void* stream);
 
 /*
  * CUDA IPC plumbing for the symmetric buffers (host calls, no stream work).

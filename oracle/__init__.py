@@ -33,6 +33,7 @@ from .sq_oracle import (  # noqa: F401
     smooth_weight_exact,
     fold,
     rz_fp16,
+    rn_bf16_bits,
     rha,
     quantize_group,
     quantize_pack,

@@ -5,7 +5,7 @@
 // through CUDA IPC, i.e. NVLink/NVSwitch loads and stores between GPUs):
 //
 //   [header 128 B: epoch counter, done counter][flags: 2 parities x world x kArMaxChunks
-//    uint32][slots: 2 parities x world x n_max 16-bit]
+//    uint32][slots: 2 parities x world x n_max elements, 4-byte stride] (sq_internal.cuh)
 //
 // Call `epoch` e on rank r (e > 0 given by the caller, +1 per call; or e == 0: taken from
 // the rank's own device counter + 1 and stored back by the last CTA, so a CUDA graph that
@@ -30,7 +30,6 @@ namespace sq {
 namespace {
 
 constexpr int kArThreads = 256;
-constexpr size_t kArHeaderBytes = 128;
 constexpr int kArChunkVec = kArThreads;           // 16-B vectors per chunk (4 KB of outputs)
 constexpr int kArChunkElems = kArChunkVec * 8;    // 2048 fp16 / bf16 outputs per chunk
 
@@ -68,12 +67,11 @@ oneshot_allreduce_kernel(const uint16_t* y_local, uint16_t* y_out, int64_t n,  /
   const int par = epoch & 1;
   const int64_t e0 = (int64_t)c * kArChunkElems;
   const int64_t e1 = min(n, e0 + kArChunkElems);
-  const size_t flag_bytes = kArHeaderBytes + (size_t)2 * world * kArMaxChunks * sizeof(uint32_t);
   auto flags_of = [&](uint8_t* base) {
-    return reinterpret_cast<uint32_t*>(base + kArHeaderBytes) + (size_t)par * world * kArMaxChunks;
+    return reinterpret_cast<uint32_t*>(base + ar_flags_offset()) + (size_t)par * world * kArMaxChunks;
   };
   auto slots_of = [&](uint8_t* base, int q) {
-    return reinterpret_cast<uint16_t*>(base + flag_bytes) + ((size_t)par * world + q) * n_max;
+    return reinterpret_cast<uint16_t*>(base + ar_slot_offset(world, par, q, n_max));
   };
   // 1. push this rank's chunk to every rank's slot [par][rank]
   const int64_t i = e0 + (int64_t)threadIdx.x * 8;
@@ -111,9 +109,10 @@ oneshot_allreduce_kernel(const uint16_t* y_local, uint16_t* y_out, int64_t n,  /
     }
   }
   __syncthreads();
-  if (timed_out) return;  // (the device epoch is not advanced: the collective is broken)
-  // 4. reduce in rank order (bit-identical on every rank)
-  if (i < e1) {
+  // 4. reduce in rank order (bit-identical on every rank); skipped after a timeout (the
+  //    error word reports it), but the CTA still counts itself done below so the header
+  //    stays consistent for the next call
+  if (i < e1 && !timed_out) {
     float acc[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc[t] = 0.0f;
@@ -152,10 +151,7 @@ oneshot_allreduce_kernel(const uint16_t* y_local, uint16_t* y_out, int64_t n,  /
 
 int64_t ar_chunk_elems() { return kArChunkElems; }
 
-size_t ar_buffer_bytes(int64_t n_max, int world) {
-  return kArHeaderBytes + (size_t)2 * world * kArMaxChunks * sizeof(uint32_t) +
-         (size_t)2 * world * n_max * sizeof(uint16_t);
-}
+size_t ar_buffer_bytes(int64_t n_max, int world) { return ar_slot_offset(world, 2, 0, n_max); }
 
 cudaError_t launch_oneshot_allreduce(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,
                                      void* const* peers_dev, int rank, int world, uint32_t epoch, int* err,

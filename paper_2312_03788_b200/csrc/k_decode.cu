@@ -17,8 +17,8 @@
 //    supplied in registers), so a stage is 17.5 KB instead of 24.5 KB.
 //  * Four consumer warps: warp w takes group w of every stage for all BN rows, so
 //    its X fragment is loaded (and k-permuted with PRMT) once and reused BN/16
-//    times (SQ_DEC_CW = 8 splits the rows over two warps per group instead).  Codes
-//    are turned into the EXACT integer (q - Z) in fp16/bf16 with the lop3 magic-number trick and fed to mma.sync.m16n8k16 with fp32 accumulation;
+//    times.  Codes are turned into the EXACT integer (q - Z) in fp16/bf16 with the
+//    lop3 magic-number trick and fed to mma.sync.m16n8k16 with fp32 accumulation;
 //    Δ is applied once per group to the accumulator fragment.
 //  * At the end of a row-block segment the consumer warps park their fp32 partial
 //    sums in SMEM (over their own, already consumed, activation slice of the stage)
@@ -38,76 +38,27 @@ namespace sq {
 namespace {
 
 constexpr int kGroup = 128;
-#ifndef SQ_DEC_CTAS
-#define SQ_DEC_CTAS 2
-#endif
-#ifndef SQ_DEC_SX
-#define SQ_DEC_SX 0  // 1: magic-offset codes straight into the MMA + activation-sum correction
-#endif
-#ifndef SQ_DEC_SLEEP_NS
-#define SQ_DEC_SLEEP_NS 100000  // try_wait suspend-time hint of the producer / epilogue waits
-#endif
-#ifndef SQ_DEC_ABLATE
-#define SQ_DEC_ABLATE 0  // experiment only: 1 = skip the MMAs, 2 = skip the dequant, 8 = no global epilogue,
-                         // 32 = no per-stage compute (pipeline skeleton)
-#endif
-#ifndef SQ_DEC_CW
-#define SQ_DEC_CW 4  // consumer warps: GPS groups x (SQ_DEC_CW / GPS) row slices of a stage
-                     // (8 = two warps per group: measured slower, kept as a tuning knob)
-#endif
-#ifndef SQ_DEC_TRACE
-#define SQ_DEC_TRACE 0  // development: per-CTA globaltimer trace (sq_debug_decode_trace)
-#endif
-#if SQ_DEC_TRACE
-__device__ long long* g_dec_trace = nullptr;  // [tickets][8]
-__device__ int g_dec_ticket = 0;
-__device__ __forceinline__ long long gtime() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
-  return t;
-}
-#endif
-constexpr int GPS = 4;          // groups per stage
-constexpr int kConsumerWarps = SQ_DEC_CW;
-constexpr int kRowSplit = kConsumerWarps / GPS;  // warps sharing one group's rows
-static_assert(kRowSplit * GPS == kConsumerWarps, "consumer warps must be a multiple of GPS");
-// warp roles (Cfg): consumers 0 .. CW-1, TMA producer CW, epilogue CW + 1
-#ifndef SQ_DEC_CTAS_M1
-#define SQ_DEC_CTAS_M1 2  // CTAs per SM of the M = 1 kernel (1-token activation box; 3 measured slower)
-#endif
-#ifndef SQ_DEC_SK_BN
-#define SQ_DEC_SK_BN 0  // stream-K row-block height: 0 = by shape (AUTO), 32 / 64 forced
-#endif
-#ifndef SQ_DEC_M1_CT3
-#define SQ_DEC_M1_CT3 1  // M = 1: 3 CTAs per SM for 32-64 MB layers that would stream-K
-#endif
-#ifndef SQ_DEC_EVICT_FIRST
-#define SQ_DEC_EVICT_FIRST 1  // codes TMA with an L2 evict-first policy
-#endif
-#ifndef SQ_DEC_XR4
-#define SQ_DEC_XR4 0  // 1: M = 2..4 stage 4 activation rows instead of 8 (measured -3..+5 %, net ~0)
-#endif
-#ifndef SQ_DEC_CTAS_M16
-#define SQ_DEC_CTAS_M16 2  // M = 9..16; 1 = one CTA per SM, 128-row blocks, 8 consumer warps (measured 2-35 % slower)
-#endif
-constexpr int kMaxCtasPerSm0 = SQ_DEC_CTAS > SQ_DEC_CTAS_M1 ? SQ_DEC_CTAS : SQ_DEC_CTAS_M1;
-// workspace partial slots are sized for the most CTAs any decode launch can have
-constexpr int kMaxCtasPerSm = SQ_DEC_M1_CT3 && kMaxCtasPerSm0 < 3 ? 3 : kMaxCtasPerSm0;
-constexpr int kMaxBN = 128;     // row-block heights: 32 or 64 (2 CTAs/SM), 128 (1 CTA/SM)
+constexpr int GPS = 4;             // groups per stage (unit)
+constexpr int kConsumerWarps = 4;  // one per group of a stage; warp roles: consumers 0..3, TMA producer 4, epilogue 5
+constexpr int kCtasPerSm = 2;      // M >= 2 (and M = 1 outside the 3-CTA rule): two ~112-KB CTAs per SM
+// M = 1: three 74-KB CTAs per SM for 32-64 MB layers that two CTAs would stream-K (7B gate|up -12 %,
+// 34B qkv -1-2 %; profiles/decode_m1_ct3_ab_r01.jsonl)
+constexpr int kMaxCtasPerSm = 3;   // workspace partial slots are sized for the most CTAs a launch can have
+constexpr int kMaxBN = 64;         // row-block heights: 32 or 64
 constexpr int kMinBN = 32;
+// try_wait suspend-time hint of the producer / epilogue waits (ns)
+constexpr uint32_t kIdleWaitNs = 100000;
 
 // MT: 8-token MMA n-tiles; XR: token rows of the activation box actually staged (M = 1 stages
 // one row, the MMA sees zeros for the other seven); CT: resident CTAs per SM (smem budget)
 template <int MT, int BN, int XR, int CT>
 struct Cfg {
   static constexpr int MPAD = 8 * MT;
-  // one CTA per SM: 8 consumer warps (two per group, row split) over 128-row blocks
-  static constexpr int CW = CT == 1 ? 8 : kConsumerWarps;
-  static constexpr int RS = CW / GPS;
+  static constexpr int CW = kConsumerWarps;
   static constexpr int THREADS = (CW + 2) * 32;
-  static constexpr int kSmemBudget = (CT == 1 ? 220 : CT == 2 ? 112 : 74) * 1024;  // per CTA
-  static constexpr int RT = BN / 16 / RS;                 // 16-row tiles per consumer warp
-  static_assert(RT >= 1, "row block too short for the consumer split");
+  static_assert(CT == 2 || CT == 3, "two or three CTAs per SM");
+  static constexpr int kSmemBudget = (CT == 2 ? 112 : 74) * 1024;  // per CTA
+  static constexpr int RT = BN / 16;                      // 16-row tiles per consumer warp
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
   static constexpr int XB = GPS * XR * kGroup * 2;        // 1 / 8 / 16 KB
   static constexpr int SZ = GPS * BN * 2;
@@ -119,7 +70,7 @@ struct Cfg {
   // own group's activation slice of the stage, which only that warp reads.
   static constexpr int XSLICE = XB / GPS;
   // partial sums are parked over the group's activation slice, or over its codes slab when
-  // the slice is too small (128-row blocks); both were fully read before the park
+  // the slice is too small (M = 1 stages one token row); both were fully read before the park
   static constexpr bool kParkCodes = XR * BN * 4 > XSLICE;
   static constexpr int PARK_OFF = kParkCodes ? 0 : CODES;
   static constexpr int PARK_STRIDE = kParkCodes ? BN * 64 : XSLICE;
@@ -169,7 +120,7 @@ __device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
-      "r"(parity), "r"(SQ_DEC_SLEEP_NS)
+      "r"(parity), "r"(kIdleWaitNs)
       : "memory");
 }
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
@@ -387,14 +338,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 
 // Row-parallel all-reduce fused into the epilogue (sq_w4a16_gemm_allreduce; the buffer
 // layout and protocol are those of k_allreduce.cu: header, flags[2][world][kArMaxChunks],
-// fp16/bf16 slots[2][world][n_max]; here a "chunk" is a row block).  world == 0: off.
-constexpr size_t kArHdr = 128;
+// slots[2][world][n_max] with a 4-byte slot stride; here a "chunk" is a row block).
+// world == 0: off.  fp16 partials travel as fp16, bf16 partials as fp32 (SURVEY.md §8(e):
+// reduce bf16 in fp32), and the rank-ordered sum is always taken in fp32.
 __device__ __forceinline__ uint32_t* ar_flags(uint8_t* base, int world, int par) {
-  return reinterpret_cast<uint32_t*>(base + kArHdr) + (size_t)par * world * kArMaxChunks;
+  return reinterpret_cast<uint32_t*>(base + ar_flags_offset()) + (size_t)par * world * kArMaxChunks;
 }
-__device__ __forceinline__ uint16_t* ar_slots(uint8_t* base, int world, int par, int q, int64_t n_max) {
-  return reinterpret_cast<uint16_t*>(base + kArHdr + (size_t)2 * world * kArMaxChunks * sizeof(uint32_t)) +
-         ((size_t)par * world + q) * n_max;
+__device__ __forceinline__ uint8_t* ar_slot(uint8_t* base, int world, int par, int q, int64_t n_max) {
+  return base + ar_slot_offset(world, par, q, n_max);
 }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -426,21 +377,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-#if SQ_DEC_TRACE
-  __shared__ long long* tr_row;
-  if (threadIdx.x == 0) {
-    const int t = atomicAdd(&g_dec_ticket, 1);
-    tr_row = g_dec_trace ? g_dec_trace + (size_t)t * 8 : nullptr;
-    if (tr_row) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %smid;\n" : "=r"(smid));
-      tr_row[0] = gtime();
-      tr_row[4] = smid;
-      tr_row[5] = blockIdx.x;
-    }
-  }
-  __syncthreads();
-#endif
   // the next kernel in the stream may start its prologue as our CTAs retire
   pdl_launch_dependents();
 
@@ -451,18 +387,18 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       prefetch_tmap(&tm_x);
       prefetch_tmap(&tm_s);
       prefetch_tmap(&tm_z);
-      const uint64_t wpol = SQ_DEC_EVICT_FIRST ? l2_evict_first_policy() : 0;
+      // codes are streamed exactly once: L2 evict-first keeps the activations and the
+      // stream-K partials resident (0.3-2 %, profiles/decode_evict_first_ab_r01.jsonl)
+      const uint64_t wpol = l2_evict_first_policy();
       auto load_weights = [&](uint32_t st, uint32_t fb, int u) {
         const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
-        if (SQ_DEC_EVICT_FIRST)
-          tma_3d_hint(st, &tm_w, fb, 0, rb * BN, g0, wpol);
-        else
-          tma_3d(st, &tm_w, fb, 0, rb * BN, g0);
+        tma_3d_hint(st, &tm_w, fb, 0, rb * BN, g0, wpol);
         tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
         tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
       };
       // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
-      // declared them static: stream the first stages before waiting on it.
+      // declared them static (SQ_GEMM_WEIGHTS_STATIC): stream the first stages before
+      // waiting on it.
       int pre = 0;
       if (early_weights) {
         Sched sc(wk, c, P);
@@ -473,9 +409,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
-#if SQ_DEC_TRACE
-      if (tr_row) tr_row[6] = gtime();
-#endif
       int s = 0;
       uint32_t ph = 0;
       int i = 0;
@@ -515,6 +448,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     int n_fin = 0;
     uint32_t epoch = ar.epoch;
     if (kAR && epoch == 0) {
+      // the device-managed epoch is advanced by the previous call's last CTA: read it only
+      // after that grid has completed (PDL lets this kernel start while it still runs)
+      pdl_wait();
+      waited = true;
       const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(ar.peers[ar.rank]);
       epoch = cur == 0xFFFFFFFFu ? 2u : cur + 1u;
     }
@@ -529,27 +466,33 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
         return;
       } else {
-      for (int p = 0; p < ar.world; ++p) {
-        uint16_t* dst = ar_slots(ar.peers[p], ar.world, par, ar.rank, ar.n_max);
+        for (int p = 0; p < ar.world; ++p) {
+          uint8_t* dst = ar_slot(ar.peers[p], ar.world, par, ar.rank, ar.n_max);
 #pragma unroll
-        for (int i = 0; i < E; ++i) {
-          const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
-          if (t < M && n0 + row < N) dst[(size_t)t * N + n0 + row] = to_out(val[i]);
+          for (int i = 0; i < E; ++i) {
+            const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
+            if (t < M && n0 + row < N) {
+              const size_t o = (size_t)t * N + n0 + row;
+              if (kBF16)
+                reinterpret_cast<float*>(dst)[o] = val[i];
+              else
+                reinterpret_cast<uint16_t*>(dst)[o] = to_out(val[i]);
+            }
+          }
         }
-      }
-      __threadfence_system();
-      __syncwarp();
-      if (lane < ar.world) {
-        uint32_t* f = ar_flags(ar.peers[lane], ar.world, par) + (size_t)ar.rank * kArMaxChunks + rb;
-        asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(f), "r"(epoch) : "memory");
-      }
-      if (n_fin < 64) {
-        if (lane == 0) fin_list[n_fin] = rb;
-      } else if (lane == 0) {
-        atomicExch(ar.err, 2);  // more finalized row blocks than the list holds
-      }
-      ++n_fin;
-      __syncwarp();
+        __threadfence_system();
+        __syncwarp();
+        if (lane < ar.world) {
+          uint32_t* f = ar_flags(ar.peers[lane], ar.world, par) + (size_t)ar.rank * kArMaxChunks + rb;
+          asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(f), "r"(epoch) : "memory");
+        }
+        if (n_fin < 64) {
+          if (lane == 0) fin_list[n_fin] = rb;
+        } else if (lane == 0) {
+          atomicExch(ar.err, 2);  // more finalized row blocks than the list holds
+        }
+        ++n_fin;
+        __syncwarp();
       }
     };
     for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
@@ -572,13 +515,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
           pdl_wait();
           waited = true;
         }
-        const int n0 = rb * BN;
-        if (SQ_DEC_ABLATE == 8) {
-          if (v[0] == 1234.5f) Y[0] = 1;
-        } else if (sc.full) {
+        if (sc.full) {
           emit(rb, v);
-        } else if (SQ_DEC_ABLATE == 16) {
-          if (v[0] == 1234.5f) Y[0] = 1;
         } else {
           // stream-K fixup: park the partial; the last contributor sums them in CTA order
           float* slot = partials + ((size_t)c * 2 + sc.e) * (16 * kMaxBN);
@@ -649,17 +587,21 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         for (int i = 0; i < E; ++i) {
           const int idx = lane + 32 * i, t = idx / BN, row = idx % BN;
           if (t < M && n0 + row < N) {
+            const size_t o = (size_t)t * N + n0 + row;
             float acc = 0.0f;
             for (int q = 0; q < ar.world; ++q) {
-              const uint16_t b = __ldcv(ar_slots(ar.peers[ar.rank], ar.world, par, q, ar.n_max) +
-                                        (size_t)t * N + n0 + row);
-              acc += kBF16 ? __bfloat162float(__ushort_as_bfloat16(b)) : __half2float(__ushort_as_half(b));
+              const uint8_t* src = ar_slot(ar.peers[ar.rank], ar.world, par, q, ar.n_max);
+              if (kBF16)
+                acc += __ldcv(reinterpret_cast<const float*>(src) + o);
+              else
+                acc += __half2float(__ushort_as_half(__ldcv(reinterpret_cast<const uint16_t*>(src) + o)));
             }
-            Y[(size_t)t * N + n0 + row] = to_out(acc);
+            Y[o] = to_out(acc);
           }
         }
       }
-      // the last CTA to finish advances the device-managed epoch
+      // the last CTA to finish advances the device-managed epoch (also after a timeout, so
+      // the header stays consistent; the error word reports the failure)
       if (ar.epoch == 0 && lane == 0) {
         uint32_t* hdr = reinterpret_cast<uint32_t*>(ar.peers[ar.rank]);
         __threadfence();
@@ -670,15 +612,12 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         }
       }
     }
-#if SQ_DEC_TRACE
-    if (lane == 0 && tr_row) tr_row[3] = gtime();
-#endif
     return;
   }
 
-  // ===== consumers: warp w = group (w % GPS), rows [roff, roff + BN / RS) of each stage =====
+  // ===== consumers: warp w = group w of each stage, all BN rows =====
   const int r = lane / 4, j = lane % 4;
-  const int grp = warp % GPS, roff = (warp / GPS) * (BN / C::RS);
+  const int grp = warp;
   float acc[C::RT][MT][4];
 #pragma unroll
   for (int rt = 0; rt < C::RT; ++rt)
@@ -689,22 +628,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   int s = 0;
   uint32_t ph = 0;
-#if SQ_DEC_TRACE
-  bool first = true;
-#endif
   for (Sched sc(wk, c, P); sc.valid(); sc.next(wk)) {
     mbar_wait(bar_full + 8 * s, ph);
-#if SQ_DEC_TRACE
-    if (first && warp == 0 && lane == 0 && tr_row) tr_row[1] = gtime();
-    first = false;
-#endif
     const uint32_t st = sbase + s * C::STAGE;
-    if (SQ_DEC_ABLATE == 32) {  // experiment: no per-stage compute at all (pipeline skeleton)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sc.range_last() ? red_full + 8 * s : bar_empty + 8 * s);
-      if (++s == C::NS) { s = 0; ph ^= 1; }
-      continue;
-    }
     // ---- X fragments of this warp's group: token t = r + 8 mt, k = 32 j + [0, 32)
     uint32_t xb[MT][4][4];
 #pragma unroll
@@ -727,28 +653,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         xb[mt][w][3] = prmt(xv[4 * w + 1], xv[4 * w + 3], 0x7632u);  // (x3, x7)
       }
     }
-    // activation sums of this group for this lane's tokens, even-k and odd-k positions
-    // (SQ_DEC_SX: the MMAs see 1024 + q, the zero point and offset are removed per group)
-    float sxe[MT][2], sxo[MT][2];
-    if (SQ_DEC_SX) {
-      const uint32_t kOnes = kBF16 ? 0x3F803F80u : 0x3C003C00u;
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        float se[4], so[4];
-        mma_16816_zc(se, kOnes, kOnes, kOnes, kOnes, xb[mt][0][0], xb[mt][0][2], kBF16);
-        mma_16816_zc(so, kOnes, kOnes, kOnes, kOnes, xb[mt][0][1], xb[mt][0][3], kBF16);
-#pragma unroll
-        for (int w = 1; w < 4; ++w) {
-          mma_16816(se, kOnes, kOnes, kOnes, kOnes, xb[mt][w][0], xb[mt][w][2], kBF16);
-          mma_16816(so, kOnes, kOnes, kOnes, kOnes, xb[mt][w][1], xb[mt][w][3], kBF16);
-        }
-        sxe[mt][0] = se[0]; sxe[mt][1] = se[1];
-        sxo[mt][0] = so[0]; sxo[mt][1] = so[1];
-      }
-    }
     // codes of this warp's group: [group][row][64 B]
-    const uint32_t cbase = st + grp * (BN * 64) + (roff + r) * 64 + j * 16;
-    const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + (roff + r) * 2;
+    const uint32_t cbase = st + grp * (BN * 64) + r * 64 + j * 16;
+    const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
     const uint32_t sbz = sbs + C::SZ;
 #pragma unroll
     for (int rt = 0; rt < C::RT; ++rt) {
@@ -758,62 +665,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       const float dB = __half2float(__ushort_as_half(lds16(sbs + rt * 32 + 16)));
       const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
       const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
-      if (SQ_DEC_SX) {
-        const float zA = __half2float(__ushort_as_half(lds16(sbz + rt * 32)));
-        const float zB = __half2float(__ushort_as_half(lds16(sbz + rt * 32 + 16)));
-        constexpr uint32_t kMagic = kBF16 ? 0x43004300u : 0x64006400u;
-        float ge[MT][4], go[MT][4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint32_t la0, la1, ha0, ha1, lb0, lb1, hb0, hb1;
-          if (!kBF16) {  // 1024 + q for the low nibbles, 1024 + 16 q for the high ones
-            const uint32_t ta = wa[w] >> 8, tb = wb[w] >> 8;
-            la0 = lop3_and_or(wa[w], 0x000F000Fu, kMagic);
-            la1 = lop3_and_or(ta, 0x000F000Fu, kMagic);
-            ha0 = lop3_and_or(wa[w], 0x00F000F0u, kMagic);
-            ha1 = lop3_and_or(ta, 0x00F000F0u, kMagic);
-            lb0 = lop3_and_or(wb[w], 0x000F000Fu, kMagic);
-            lb1 = lop3_and_or(tb, 0x000F000Fu, kMagic);
-            hb0 = lop3_and_or(wb[w], 0x00F000F0u, kMagic);
-            hb1 = lop3_and_or(tb, 0x00F000F0u, kMagic);
-          } else {       // 128 + q (bf16 has too few mantissa bits for 128 + 16 q)
-            la0 = lop3_and_or(wa[w], 0x000F000Fu, kMagic);
-            la1 = lop3_and_or(wa[w] >> 8, 0x000F000Fu, kMagic);
-            ha0 = lop3_and_or(wa[w] >> 4, 0x000F000Fu, kMagic);
-            ha1 = lop3_and_or(wa[w] >> 12, 0x000F000Fu, kMagic);
-            lb0 = lop3_and_or(wb[w], 0x000F000Fu, kMagic);
-            lb1 = lop3_and_or(wb[w] >> 8, 0x000F000Fu, kMagic);
-            hb0 = lop3_and_or(wb[w] >> 4, 0x000F000Fu, kMagic);
-            hb1 = lop3_and_or(wb[w] >> 12, 0x000F000Fu, kMagic);
-          }
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            if (w == 0) {
-              mma_16816_zc(ge[mt], la0, lb0, la1, lb1, xb[mt][w][0], xb[mt][w][2], kBF16);
-              mma_16816_zc(go[mt], ha0, hb0, ha1, hb1, xb[mt][w][1], xb[mt][w][3], kBF16);
-            } else {
-              mma_16816(ge[mt], la0, lb0, la1, lb1, xb[mt][w][0], xb[mt][w][2], kBF16);
-              mma_16816(go[mt], ha0, hb0, ha1, hb1, xb[mt][w][1], xb[mt][w][3], kBF16);
-            }
-          }
-        }
-        // sum_k X (q - Z) = ge + go/16 - (1024+Z) SXe - (64+Z) SXo   (fp16 magic)
-        //                 = ge + go    - (128+Z) (SXe + SXo)          (bf16 magic)
-        const float osc = kBF16 ? 1.0f : 0.0625f;
-        const float ceA = -((kBF16 ? 128.0f : 1024.0f) + zA), coA = -((kBF16 ? 128.0f : 64.0f) + zA);
-        const float ceB = -((kBF16 ? 128.0f : 1024.0f) + zB), coB = -((kBF16 ? 128.0f : 64.0f) + zB);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float ce = i < 2 ? ceA : ceB, co = i < 2 ? coA : coB, d = i < 2 ? dA : dB;
-            float v = fmaf(go[mt][i], osc, ge[mt][i]);
-            v = fmaf(ce, sxe[mt][i & 1], v);
-            v = fmaf(co, sxo[mt][i & 1], v);
-            acc[rt][mt][i] = fmaf(v, d, acc[rt][mt][i]);
-          }
-        continue;
-      }
       uint32_t zsA, zfA, zsB, zfB;
       zero_consts<kBF16>(lds16(sbz + rt * 32), zsA, zfA);
       zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB, zfB);
@@ -821,22 +672,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t hA[4], hB[4];
-        if (SQ_DEC_ABLATE == 2) {
-          hA[0] = wa[w]; hA[1] = wa[w] >> 8; hA[2] = wa[w] >> 4; hA[3] = wa[w] >> 12;
-          hB[0] = wb[w]; hB[1] = wb[w] >> 8; hB[2] = wb[w] >> 4; hB[3] = wb[w] >> 12;
-        } else {
-          dequant_word<kBF16>(wa[w], zsA, zfA, hA);
-          dequant_word<kBF16>(wb[w], zsB, zfB, hB);
-        }
+        dequant_word<kBF16>(wa[w], zsA, zfA, hA);
+        dequant_word<kBF16>(wb[w], zsB, zfB, hB);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          if (SQ_DEC_ABLATE == 1) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              g[mt][i] = (w == 0 ? 0.0f : g[mt][i]) +
-                         __uint_as_float((hA[i] ^ hB[i] ^ xb[mt][w][i]) & 0x3FFFFFFFu);
-            continue;
-          }
           // A = rows (r, r+8) x k pairs; B = the same k pairs of this lane's token
           if (w == 0)
             mma_16816_zc(g[mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
@@ -862,16 +701,12 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     } else {
       // park this warp's partial sums over its own activation slice of the stage and hand
       // them to the epilogue warp, which also releases the stage; no CTA-wide barrier
-      // (the warps of one group write disjoint rows of the group's slot, after all of them
-      // have read their activation fragments from it: named barrier 1 + grp)
-      if (C::RS > 1)
-        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(32 * C::RS) : "memory");
       float* slot = reinterpret_cast<float*>(smem + s * C::STAGE + C::PARK_OFF + grp * C::PARK_STRIDE);
 #pragma unroll
       for (int rt = 0; rt < C::RT; ++rt)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const int t0 = 8 * mt + 2 * j, ra = roff + rt * 16 + r;
+          const int t0 = 8 * mt + 2 * j, ra = rt * 16 + r;
           if (XR >= C::MPAD || t0 < XR) {
             slot[t0 * BN + ra] = acc[rt][mt][0];
             slot[t0 * BN + ra + 8] = acc[rt][mt][2];
@@ -891,9 +726,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     }
     if (++s == C::NS) { s = 0; ph ^= 1; }
   }
-#if SQ_DEC_TRACE
-  if (warp == 0 && lane == 0 && tr_row) tr_row[2] = gtime();
-#endif
 }
 
 // ------------------------------------------------------------------ host side
@@ -922,11 +754,18 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Resident CTAs per SM of one kernel instance (occupancy query), cached per device: the
+// dynamic-smem attribute is per device context, so it is set on each device before use.
 template <int MT, bool kBF16, int BN, int XR, int CT>
 int ctas_per_sm() {
-  static int cached = -1;
-  if (cached < 0) {
-    int n = 0;
+  static int cached[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [] {
+    int d = 0, n = 0;
+    cudaGetDevice(&d);
     cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
     cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -935,15 +774,15 @@ int ctas_per_sm() {
                                                       Cfg<MT, BN, XR, CT>::THREADS,
                                                       Cfg<MT, BN, XR, CT>::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
-    cached = std::min(n, CT);
-  }
-  return cached;
+    cached[d < 64 && d >= 0 ? d : 0] = std::min(n, CT);
+  });
+  return cached[dev];
 }
 
 template <int MT, bool kBF16, int BN, int XR, int CT>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                     void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, cudaStream_t st,
-                     const char** why) {
+                     void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, bool weights_static,
+                     cudaStream_t st, const char** why) {
   using C = Cfg<MT, BN, XR, CT>;
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
@@ -980,7 +819,8 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   wk.upb = (G + GPS - 1) / GPS;
   wk.units = wk.rbs * wk.upb;
   wk.dp = dp ? 1 : 0;
-  const int slots = num_sms() * ctas_per_sm<MT, kBF16, BN, XR, CT>();
+  int slots = num_sms() * ctas_per_sm<MT, kBF16, BN, XR, CT>();
+  if (option(SQ_OPT_DECODE_GRID_LIMIT) > 0) slots = std::min(slots, option(SQ_OPT_DECODE_GRID_LIMIT));
   const int P = dp ? std::min(wk.rbs, slots) : std::min(wk.units, slots);
   wk.cta_q = wk.units / P;
   wk.cta_r = wk.units % P;
@@ -998,7 +838,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   attr[0].val.programmaticStreamSerializationAllowed = option(SQ_OPT_PDL) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
+  const int early = option(SQ_OPT_PDL) && weights_static;
   if (ar.world > 0)
     return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, true>, tw, tx, ts, tz, (uint16_t*)Y,
                               counters, partials, M, N, wk, early, ar);
@@ -1031,15 +871,10 @@ bool auto_rowblock(int N, int K, int slots, int* bn_out) {
 
 template <int MT, bool kBF16, int XR, int CT>
 cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                     void* Y, int M, int N, int K, void* ws, const ArParams& ar, cudaStream_t st,
-                     const char** why) {
+                     void* Y, int M, int N, int K, void* ws, const ArParams& ar, bool weights_static,
+                     cudaStream_t st, const char** why) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
   const int slots = num_sms() * CT;
-  if constexpr (CT == 1) {  // one CTA per SM: 128-row blocks, stream-K
-    (void)sched;
-    (void)slots;
-    return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, st, why);
-  } else {
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
   // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots, a CTA's
   // row block exceeds the stream-K share by at most what the fixups cost (~2.5 µs at a CTA's
@@ -1052,7 +887,7 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // stream-K row-block height: 32 rows for M = 9..16 on layers below 48 MB of codes (half
   // the cut row blocks' fixup work; measured -8..-13 % on the 7B shapes, +2 % on 34B qkv),
   // 64 otherwise (larger stages stream faster)
-  int bn = SQ_DEC_SK_BN ? SQ_DEC_SK_BN : (MT == 2 && (double)N * K / 2 < 48.0 * 1024 * 1024 ? 32 : 64);
+  int bn = MT == 2 && (double)N * K / 2 < 48.0 * 1024 * 1024 ? 32 : 64;
   if (sched == SQ_SCHED_ROWBLOCK) {
     bn = rowblock_utilization(N, 64, slots) >= rowblock_utilization(N, 32, slots) ? 64 : 32;
   } else if (sched == SQ_SCHED_AUTO) {
@@ -1062,9 +897,14 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
       bn = rbn;
     }
   }
-  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
-  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, st, why);
+  if (ar.world > 0) {
+    // fused all-reduce: flags are per row block, so every rank must cut N the same way.
+    // Decide from N alone (K differs between row-parallel shards): stream-K, 64-row blocks.
+    dp = false;
+    bn = 64;
   }
+  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, st, why);
+  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, st, why);
 }
 
 }  // namespace
@@ -1079,46 +919,29 @@ size_t decode_workspace_bytes(int64_t N) {
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
+                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, bool weights_static,
                           cudaStream_t st, const char** why, const ArParams* ar_in) {
   const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
-  constexpr int C2 = SQ_DEC_CTAS, C1 = SQ_DEC_CTAS_M1;
   if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
     // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
     // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
-    // measured -12 % on 7B gate|up, -2 % on 34B qkv (profiles/decode_m1_ct3_ab_r01.jsonl)
+    // measured -12 % on 7B gate|up, -2 % on 34B qkv (profiles/decode_m1_ct3_ab_r01.jsonl).
+    // Not for the fused all-reduce (its row-block cut must not depend on the rank's K).
     const double codes = (double)N * K / 2;
     int rbn = 64;
-    if (SQ_DEC_M1_CT3 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO && codes >= 32.0 * 1024 * 1024 &&
-        codes <= 64.0 * 1024 * 1024 && !auto_rowblock(N, K, num_sms() * C1, &rbn))
-      return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-                  : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
-    return bf16 ? launch_m<1, true, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-                : launch_m<1, false, 1, C1>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+    if (ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO && codes >= 32.0 * 1024 * 1024 &&
+        codes <= 64.0 * 1024 * 1024 && !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn))
+      return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
+                  : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+    return bf16 ? launch_m<1, true, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
+                : launch_m<1, false, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
   }
-#if SQ_DEC_XR4
-  if (M <= 4)  // stage four activation rows
-    return bf16 ? launch_m<1, true, 4, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-                : launch_m<1, false, 4, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
-#endif
   if (M <= 8)
-    return bf16 ? launch_m<1, true, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-                : launch_m<1, false, 8, C2>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
-  constexpr int C16 = SQ_DEC_CTAS_M16;
-  return bf16 ? launch_m<2, true, 16, C16>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why)
-              : launch_m<2, false, 16, C16>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, st, why);
+    return bf16 ? launch_m<1, true, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
+                : launch_m<1, false, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+  return bf16 ? launch_m<2, true, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
+              : launch_m<2, false, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
 }
 
 }  // namespace sq
-
-#if SQ_DEC_TRACE
-// development only: per-CTA trace rows [start, first data, consumers done, epilogue done,
-// smid, blockIdx, -, -] in launch-ticket order (ticket counter reset by this call)
-extern "C" __attribute__((visibility("default"))) int sq_debug_decode_trace(void* dev_buf) {
-  long long* p = static_cast<long long*>(dev_buf);
-  int z = 0;
-  if (cudaMemcpyToSymbol(sq::g_dec_trace, &p, sizeof(p)) != cudaSuccess) return 1;
-  return cudaMemcpyToSymbol(sq::g_dec_ticket, &z, sizeof(z)) != cudaSuccess;
-}
-#endif

@@ -31,33 +31,21 @@ namespace sq {
 
 namespace {
 
-#ifndef SQ_PRE_2CTA
-#define SQ_PRE_2CTA 0  // 1: CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles)
-#endif
 constexpr int BM = 128;        // weight rows per tile (MMA M, TMEM lanes)
 constexpr int BT = 256;        // tokens per tile (MMA N max)
 constexpr int BK = 64;         // k per X stage / A stage
 constexpr int kGroup = 128;
 constexpr int NSX = 4;         // X stages (SMEM)
 constexpr int NSC = 8;         // code+scale stages (SMEM), one group each
-#ifndef SQ_PRE_NSA
-#define SQ_PRE_NSA 4
-#endif
-constexpr int NSA = SQ_PRE_NSA;  // dequantized-A stages (TMEM, 32 columns each; D + A <= 512)
-#ifndef SQ_PRE_DQW
-#define SQ_PRE_DQW 8  // dequant/epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter)
-#endif
-constexpr int kDQW = SQ_PRE_DQW;
+constexpr int NSA = 4;         // dequantized-A stages (TMEM, 32 columns each; D + A <= 512)
+constexpr int kDQW = 8;        // dequant/epilogue warps: two per TMEM lane quarter
 constexpr int kDequantWarp0 = 4;
 constexpr int kThreads = (kDequantWarp0 + kDQW) * 32;
 constexpr int kColSplit = kDQW / 4;  // warps sharing a lane quarter split the work / token columns
-#ifndef SQ_PRE_STAGESPLIT
-#define SQ_PRE_STAGESPLIT 1
-#endif
 // 8 dequant warps: the two warps of a lane quarter take alternate 64-k stages (k-halves of
 // each group) instead of the two 32-k halves of every stage, so two A stages are in flight
 // at once and the tcgen05.st -> wait::st -> arrive latency of one overlaps the other's math
-constexpr bool kStageSplit = SQ_PRE_STAGESPLIT && kColSplit == 2;
+constexpr bool kStageSplit = kColSplit == 2;
 constexpr int kAFullCount = kStageSplit ? kDQW / 2 : kDQW;
 
 constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
@@ -92,34 +80,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
-#ifndef SQ_PRE_ABLATE
-#define SQ_PRE_ABLATE 0  // development: 1 = no X loads, 2 = no code loads, 4 = no dequant (timing only)
-#endif
-#ifndef SQ_PRE_TRACE
-#define SQ_PRE_TRACE 0  // development: per-CTA cycles spent in each barrier wait
-#endif
-#if SQ_PRE_TRACE
-__device__ unsigned long long g_pre_trace[1024 * 8];
-#define PTW(slot, call)                   \
-  do {                                    \
-    const long long t_ = clock64();       \
-    call;                                 \
-    tr[slot] += clock64() - t_;           \
-  } while (0)
-#else
-#define PTW(slot, call) call
-#endif
-#if SQ_PRE_TRACE
-__device__ long long g_pre_ts[16 * 1024];
-#define PTS(row, idx)                                                              \
-  do {                                                                              \
-    if (blockIdx.x == 0 && (idx) < 1024) g_pre_ts[(row) * 1024 + (idx)] = clock64(); \
-  } while (0)
-#else
-#define PTS(row, idx) \
-  do {                \
-  } while (0)
-#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -246,7 +206,11 @@ __device__ __forceinline__ uint32_t hmul2_f16(uint32_t a, uint32_t b) {
 
 // 8 codes (k0..k7, natural order) of one row -> 4 words of Ŵ = RN((q - Z) Δ) pairs
 // (k0,k1), (k2,k3), (k4,k5), (k6,k7) in the MMA's natural k order.
-template <bool kBF16>
+// kSat (fp16 only, groups with Δ > 65504 / 15): |(q - Z) Δ| may exceed the fp16 range, so
+// the product is formed in fp32 (exact: 5 x 11 bits) and rounded with saturation to
+// ±65504 instead of overflowing to Inf (include/libsq.h).  Never taken for real weights
+// (|W| < 2.5); the branch is per (row, group), uniform in practice.
+template <bool kBF16, bool kSat = false>
 __device__ __forceinline__ void dequant8(uint32_t w, uint32_t zc, uint32_t d2, float df,
                                          uint32_t* out) {
   const uint32_t u = w >> 4;
@@ -256,7 +220,13 @@ __device__ __forceinline__ void dequant8(uint32_t w, uint32_t zc, uint32_t d2, f
     // low nibble of w.byte(i) -> half 0, low nibble of (w>>4).byte(i) -> half 1
     const uint32_t p = lop3_and_or(prmt(w, u, sel[i]), 0x000F000Fu, 0x64006400u);
     const uint32_t qz = hsub2_f16(p, zc);  // exact (q - Z) in fp16
-    if (!kBF16) {
+    if (!kBF16 && kSat) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qz));
+      const float lo = fminf(fmaxf(f.x * df, -65504.0f), 65504.0f);
+      const float hi = fminf(fmaxf(f.y * df, -65504.0f), 65504.0f);
+      const __half2 h = __floats2half2_rn(lo, hi);  // RN of the clamped exact product
+      out[i] = *reinterpret_cast<const uint32_t*>(&h);
+    } else if (!kBF16) {
       out[i] = hmul2_f16(qz, d2);           // RN16((q - Z) Δ)
     } else {
       const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qz));
@@ -375,13 +345,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const int m0 = (tile % m_tiles) * BT;
         for (int kb = 2 * sc.g0; kb < 2 * sc.g1; ++kb) {
           mbar_wait(x_empty(xs), xph ^ 1);
-          PTS(5, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
-          if (SQ_PRE_ABLATE & 1) {
-            mbar_arrive(x_full(xs));
-          } else {
-            mbar_expect_tx(x_full(xs), x_bytes);
-            tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
-          }
+          mbar_expect_tx(x_full(xs), x_bytes);
+          tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
           if (++xs == NSX) { xs = 0; xph ^= 1; }
         }
       }
@@ -397,15 +362,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const int n0 = (tile / m_tiles) * BM;
         for (int g = sc.g0; g < sc.g1; ++g) {
           mbar_wait(c_empty(cs), cph ^ 1);
-          PTS(4, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
-          if (SQ_PRE_ABLATE & 2) {
-            mbar_arrive(c_full(cs));
-          } else {
-            mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
-            tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
-            tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
-            tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
-          }
+          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
+          tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
+          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
+          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
           if (++cs == NSC) { cs = 0; cph ^= 1; }
         }
       }
@@ -415,24 +375,18 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     {
       int xs = 0, as = 0;
       uint32_t xph = 0, aph = 0, dph = 0;
-#if SQ_PRE_TRACE
-      unsigned long long tr[4] = {0, 0, 0, 0};
-      const long long t_all = clock64();
-#endif
       for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
         const int tile = sc.tile;
         const int m0 = (tile % m_tiles) * BT;
         const int n_mma = min(BT, ((M - m0) + 15) & ~15);
         const uint32_t idesc = make_idesc(kBF16, n_mma);
-        PTW(0, mbar_wait(d_empty, dph ^ 1));  // epilogue has drained the accumulator
+        mbar_wait(d_empty, dph ^ 1);  // epilogue has drained the accumulator
         dph ^= 1;
         tc_fence_after();
         const int kb0 = 2 * sc.g0;
         for (int kb = kb0; kb < 2 * sc.g1; ++kb) {
-          PTW(1, mbar_wait(a_full(as), aph));
-          PTS(0, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
-          PTW(2, mbar_wait(x_full(xs), xph));
-          PTS(1, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + kb);
+          mbar_wait(a_full(as), aph);
+          mbar_wait(x_full(xs), xph);
           tc_fence_after();
           const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE_BYTES;
 #pragma unroll
@@ -448,10 +402,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         }
         tc_commit(d_full);
       }
-#if SQ_PRE_TRACE
-      tr[3] = clock64() - t_all;
-      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + i] = tr[i];
-#endif
     }
   } else if (warp >= kDequantWarp0) {
     // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
@@ -462,11 +412,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     int cs = 0, as = 0;
     uint32_t cph = 0, aph = 0, dph = 0;
     int ai = 0;  // A-ring stage counter (stage-split mode)
-#if SQ_PRE_TRACE
-    unsigned long long tr[4] = {0, 0, 0, 0};
-    const long long t_all = clock64();
-#endif
-    uint32_t abl_sink = 0;
     for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
       const int tile = sc.tile;
       const int n0 = (tile / m_tiles) * BM;
@@ -490,8 +435,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           const float df = __half2float(__ushort_as_half(sbits));
           const uint32_t words[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
           uint32_t a[32];
+if (!kBF16 && df > 4366.0f) {
 #pragma unroll
-          for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+            for (int wd = 0; wd < 8; ++wd) dequant8<kBF16, true>(words[wd], zc, d2, df, &a[4 * wd]);
+          } else {
+#pragma unroll
+            for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+          }
           // this warp's stage: k-half ch of the group -> A-ring index ai + ch
           const int i = ai + ch;
           const int slot = i % NSA;
@@ -505,8 +455,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           ai += 2;
           continue;
         }
-        PTW(0, mbar_wait(c_full(cs), cph));
-        if (lane == 0 && warp == kDequantWarp0) PTS(2, ((tile - (int)blockIdx.x) / (int)gridDim.x) * G + g);
+        mbar_wait(c_full(cs), cph);
         const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
         // SWIZZLE_64B: 16-byte chunk c of this row sits at chunk c ^ ((row >> 1) & 3)
         const int sw = (row >> 1) & 3;
@@ -541,26 +490,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
             words[4 * c] = v.x; words[4 * c + 1] = v.y; words[4 * c + 2] = v.z; words[4 * c + 3] = v.w;
           }
           uint32_t a[4 * kW];
-          if (SQ_PRE_ABLATE & 16) {
+if (!kBF16 && df > 4366.0f) {
 #pragma unroll
-            for (int i = 0; i < 4 * kW; ++i) a[i] = words[i % kW] + i;
+            for (int wd = 0; wd < kW; ++wd) dequant8<kBF16, true>(words[wd], zc, d2, df, &a[4 * wd]);
           } else {
 #pragma unroll
             for (int wd = 0; wd < kW; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
           }
-          PTW(1, mbar_wait(a_empty(as), aph ^ 1));
-          if (lane == 0 && warp == kDequantWarp0)
-            PTS(3, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + 2 * g + h);
-          if (SQ_PRE_ABLATE & 8) {
-#pragma unroll
-            for (int i = 0; i < 4 * kW; ++i) abl_sink ^= a[i];
-          }
-          if (SQ_PRE_ABLATE & 12) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(a_full(as));
-            if (++as == NSA) { as = 0; aph ^= 1; }
-            continue;
-          }
+          mbar_wait(a_empty(as), aph ^ 1);
           tc_fence_after();
           if constexpr (kColSplit == 1)
             tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2),
@@ -571,18 +508,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(a_full(as));
-          if (lane == 0)
-            PTS(6 + warp - kDequantWarp0, ((tile - (int)blockIdx.x) / (int)gridDim.x) * num_kb + 2 * g + h);
           if (++as == NSA) { as = 0; aph ^= 1; }
         }
       }
       // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
       pdl_wait();  // (returns at once after the first tile) Y may be read by the previous kernel
-      PTW(2, mbar_wait(d_full, dph));
+      mbar_wait(d_full, dph);
       dph ^= 1;
-#if SQ_PRE_TRACE
-      const long long t_ep = clock64();
-#endif
       tc_fence_after();
       const int n = n0 + row;
       const int mt = min(BT, M - m0);
@@ -649,17 +581,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");  // flag reuse
       }
-#if SQ_PRE_TRACE
-      tr[3] += clock64() - t_ep;
-#endif
     }
-    if ((SQ_PRE_ABLATE & 8) && abl_sink == 0x9E3779B9u) Y[0] = 1;
-#if SQ_PRE_TRACE
-    if (warp == kDequantWarp0 && lane == 0)
-      for (int i = 0; i < 3; ++i) g_pre_trace[blockIdx.x * 8 + 4 + i] = tr[i];
-    if (warp == kDequantWarp0 && lane == 0) g_pre_trace[blockIdx.x * 8 + 7] = tr[3];
-    (void)t_all;
-#endif
   }
 
   tc_fence_before();
@@ -667,322 +589,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
-  }
-}
-
-// ------------------------------------------------------------------ 2-CTA (CTA-pair) variant
-// Same dataflow, but a cluster of two CTAs on a TPC computes a 256-row x 256-token tile
-// with tcgen05.mma.cta_group::2 (M = 256): each CTA dequantizes its own 128 weight rows
-// into its own TMEM and loads half of the token tile into its own shared memory, so
-// every SM reads and writes half the activation bytes per MMA -- the 1-CTA kernel is
-// shared-memory-bandwidth bound on the X operand (TMA write + MMA read).
-namespace p2 {
-constexpr int BT2 = 256;                           // tokens per tile (MMA N)
-constexpr int NSX = 6;
-constexpr int NSC = 8;
-constexpr int NSA = SQ_PRE_NSA;
-constexpr int X_STAGE = (BT2 / 2) * BK * 2;        // 16 KB: this CTA's half of the tokens
-constexpr int OFF_X = 0;
-constexpr int OFF_C = OFF_X + NSX * X_STAGE;
-constexpr int OFF_S = OFF_C + NSC * C_STAGE_BYTES;
-constexpr int OFF_Z = OFF_S + NSC * SZ_BYTES;
-constexpr int OFF_BAR = OFF_Z + NSC * SZ_BYTES;
-constexpr int NUM_BARS = 2 * NSX + 2 * NSC + 2 * NSA + 2;
-constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
-constexpr int SMEM = OFF_TMEM + 16;
-constexpr int SMEM_ALLOC = SMEM + 1024;
-}  // namespace p2
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// arrive on the barrier at the same offset in CTA 0 of the pair (bit 24 of a
-// shared::cluster address selects the peer CTA)
-__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
-  // default (.release.cta) semantics: no GPU-scope membar; the TMEM data is ordered by
-  // tcgen05.wait::st + tcgen05.fence::before_thread_sync before this arrive
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar & 0xFEFFFFFFu) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                                 int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-      "[%1, {%3, %4}], [%2];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
-  asm volatile(
-      "{\n.reg .b16 m;\n.reg .pred e;\nmov.b16 m, 3;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n"
-      ::"r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                               uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e, p;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-
-template <bool kBF16>
-__global__ void __launch_bounds__(kThreads, 1)
-prefill2_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
-                uint16_t* __restrict__ Y, int M, int N, int K, int early_weights) {
-  constexpr int NSX = p2::NSX, NSC = p2::NSC, NSA = p2::NSA, BT2 = p2::BT2, X_STAGE = p2::X_STAGE;
-  constexpr int OFF_X = p2::OFF_X, OFF_C = p2::OFF_C, OFF_S = p2::OFF_S, OFF_Z = p2::OFF_Z;
-  constexpr int OFF_BAR = p2::OFF_BAR, OFF_TMEM = p2::OFF_TMEM;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = sbase + OFF_BAR;
-  auto x_full = [&](int i) { return bar0 + 8u * i; };
-  auto x_empty = [&](int i) { return bar0 + 8u * (NSX + i); };
-  auto c_full = [&](int i) { return bar0 + 8u * (2 * NSX + i); };
-  auto c_empty = [&](int i) { return bar0 + 8u * (2 * NSX + NSC + i); };
-  auto a_full = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + i); };
-  auto a_empty = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + NSA + i); };
-  const uint32_t d_full = bar0 + 8u * (2 * NSX + 2 * NSC + 2 * NSA);
-  const uint32_t d_empty = d_full + 8u;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / 2, num_clusters = gridDim.x / 2;
-  const int n_tiles = (N + 2 * BM - 1) / (2 * BM);
-  const int m_tiles = (M + BT2 - 1) / BT2;
-  const int num_tiles = n_tiles * m_tiles;
-  const int num_kb = K / BK;
-  const int G = K / kGroup;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
-    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), kDQW); }
-    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), 2 * kDQW); mbar_init(a_empty(i), 1); }
-    mbar_init(d_full, 1);
-    mbar_init(d_empty, 2 * kDQW);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_x);
-    prefetch_tmap(&tm_w);
-    prefetch_tmap(&tm_s);
-    prefetch_tmap(&tm_z);
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-  }
-  tc_fence_before();
-  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-  pdl_launch_dependents();
-
-  auto tile_n_mma = [&](int m0) { return min(BT2, ((M - m0) + 31) & ~31); };
-
-  if (warp == 0) {
-    // ===================== TMA producer: this CTA's half of the token tile =====================
-    if (lane == 0) {
-      pdl_wait();
-      int xs = 0;
-      uint32_t xph = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int m0 = (tile % m_tiles) * BT2;
-        const int half = tile_n_mma(m0) / 2;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(x_empty(xs), xph ^ 1);
-          if (leader) mbar_expect_tx(x_full(xs), 2 * X_STAGE);
-          tma_load_2d_pair(sbase + OFF_X + xs * X_STAGE, &tm_x, x_full(xs), kb * BK,
-                           m0 + (int)rank * half);
-          if (++xs == NSX) { xs = 0; xph ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 2) {
-    // ===================== TMA producer: this CTA's 128 weight rows =====================
-    if (lane == 0) {
-      if (!early_weights) pdl_wait();
-      int cs = 0;
-      uint32_t cph = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int n0 = (tile / m_tiles) * 2 * BM + (int)rank * BM;
-        for (int g = 0; g < G; ++g) {
-          mbar_wait(c_empty(cs), cph ^ 1);
-          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
-          tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
-          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
-          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
-          if (++cs == NSC) { cs = 0; cph ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer: the leader CTA's warp (elect.sync issues) =====================
-    if (leader) {
-      int xs = 0, as = 0;
-      uint32_t xph = 0, aph = 0, dph = 0;
-#if SQ_PRE_TRACE
-      unsigned long long tr[4] = {0, 0, 0, 0};
-      const long long t_all = clock64();
-#endif
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int m0 = (tile % m_tiles) * BT2;
-        const int n_mma = tile_n_mma(m0);
-        uint32_t idesc = make_idesc(kBF16, n_mma);
-        idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(2 * BM >> 4) << 24);  // M = 256
-        PTW(0, mbar_wait(d_empty, dph ^ 1));  // both epilogues have drained the accumulators
-        dph ^= 1;
-        tc_fence_after();
-        for (int kb = 0; kb < num_kb; ++kb) {
-          PTW(1, mbar_wait(a_full(as), aph));
-          PTW(2, mbar_wait(x_full(xs), xph));
-          tc_fence_after();
-          const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t a_tmem = tmem_base + A_COL + (uint32_t)as * (BK / 2) + (uint32_t)kk * 8;
-            tc_mma_ts_pair(tmem_base + D_COL, a_tmem, make_sw128_desc(xaddr + kk * 32), idesc,
-                           (kb | kk) ? 1u : 0u);
-          }
-          tc_commit_pair(x_empty(xs));
-          tc_commit_pair(a_empty(as));
-          if (++xs == NSX) { xs = 0; xph ^= 1; }
-          if (++as == NSA) { as = 0; aph ^= 1; }
-        }
-        tc_commit_pair(d_full);
-      }
-#if SQ_PRE_TRACE
-      tr[3] = clock64() - t_all;
-      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + i] = tr[i];
-#endif
-    }
-  } else if (warp >= kDequantWarp0) {
-    // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
-    const int q = (warp - kDequantWarp0) % 4;   // TMEM sub-partition (warp % 4)
-    const int ch = (warp - kDequantWarp0) / 4;  // column split among warps of one quarter
-    const int row = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    int cs = 0, as = 0;
-    uint32_t cph = 0, aph = 0, dph = 0;
-#if SQ_PRE_TRACE
-    unsigned long long tr[4] = {0, 0, 0, 0};
-#endif
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-      const int n0 = (tile / m_tiles) * 2 * BM + (int)rank * BM;
-      const int m0 = (tile % m_tiles) * BT2;
-      for (int g = 0; g < G; ++g) {
-        PTW(0, mbar_wait(c_full(cs), cph));
-        const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
-        const int sw = (row >> 1) & 3;
-        // this warp's 16-byte chunks of the group row: k-block h uses chunks 2h .. 2h+1,
-        // split across the kColSplit warps of this lane quarter
-        constexpr int kCh = 4 / kColSplit;
-        uint4 cv[kCh];
-#pragma unroll
-        for (int c = 0; c < kCh; ++c) {
-          const int cc = (c / (2 / kColSplit)) * 2 + (kColSplit == 2 ? ch : (c % 2));
-          cv[c] = *reinterpret_cast<const uint4*>(crow + ((cc ^ sw) << 4));
-        }
-        const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
-        const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(c_empty(cs));
-        if (++cs == NSC) { cs = 0; cph ^= 1; }
-        const __half zh = __ushort_as_half(zbits);
-        const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), zh));
-        const __half2 d2h = __half2half2(__ushort_as_half(sbits));
-        const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
-        const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
-        const float df = __half2float(__ushort_as_half(sbits));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          constexpr int kW = 8 / kColSplit;
-          uint32_t words[kW];
-#pragma unroll
-          for (int c = 0; c < kW / 4; ++c) {
-            const uint4 v = cv[h * (kW / 4) + c];
-            words[4 * c] = v.x; words[4 * c + 1] = v.y; words[4 * c + 2] = v.z; words[4 * c + 3] = v.w;
-          }
-          uint32_t a[4 * kW];
-#pragma unroll
-          for (int wd = 0; wd < kW; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
-          PTW(1, mbar_wait(a_empty(as), aph ^ 1));
-          tc_fence_after();
-          if constexpr (kColSplit == 1)
-            tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2),
-                               *reinterpret_cast<const uint32_t(*)[32]>(a));
-          else
-            tmem_st_32x32b_x16(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2) + ch * 16, a);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_leader(a_full(as));
-          if (++as == NSA) { as = 0; aph ^= 1; }
-        }
-      }
-      // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
-      pdl_wait();
-      PTW(2, mbar_wait(d_full, dph));
-      dph ^= 1;
-#if SQ_PRE_TRACE
-      const long long t_ep = clock64();
-#endif
-      tc_fence_after();
-      const int n = n0 + row;
-      const int mt = min(BT2, M - m0);
-      // warps sharing a lane quarter take alternating 16-token column blocks
-      for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
-        tmem_ld_wait();
-        if (n < N) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (c0 + i < mt) {
-              const float f = __uint_as_float(v[i]);
-              Y[(size_t)(m0 + c0 + i) * N + n] = kBF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f))
-                                                       : __half_as_ushort(__float2half_rn(f));
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(d_empty);
-#if SQ_PRE_TRACE
-      tr[3] += clock64() - t_ep;
-#endif
-    }
-#if SQ_PRE_TRACE
-    if (warp == kDequantWarp0 && lane == 0)
-      for (int i = 0; i < 4; ++i) g_pre_trace[blockIdx.x * 8 + 4 + i] = tr[i];
-#endif
-  }
-
-  tc_fence_before();
-  cluster_sync_all();  // the peer's MMAs may still read this CTA's TMEM / SMEM until here
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
                  "r"(TMEM_COLS));
   }
 }
@@ -1025,19 +631,12 @@ size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * BT * BM * sizeo
 // idle at mid M (one token tile), or > 10 % on a long-K shape at large M (down_proj at
 // M = 2048).  Elsewhere the CTAs sweeping k in lockstep share X and W tiles in L2, which
 // stream-K's staggered ranges give up (measured: o_proj/qkv at M = 2048 are faster without).
-#ifndef SQ_PRE_SK
-#define SQ_PRE_SK 1  // development: 0 = never split K between CTAs
-#endif
 bool prefill_streamk(int64_t M, int64_t N, int64_t K) {
-  if (SQ_PRE_2CTA || !SQ_PRE_SK) return false;
   const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
   const int64_t P = num_sms();
   const int64_t waves = (tiles + P - 1) / P;
   const double eff = (double)tiles / (double)(waves * P);
   if (tiles * (K / kGroup) < P) return false;
-#ifdef SQ_PRE_SK_ALWAYS
-  return eff < 0.95;
-#endif
   return M <= BT ? eff < 0.95 : (eff < 0.9 && K >= 16384);
 }
 
@@ -1049,13 +648,12 @@ size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                            const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, size_t,
-                           cudaStream_t st, const char** why) {
+                           bool weights_static, cudaStream_t st, const char** why) {
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = K / kGroup;
-  const bool pair = SQ_PRE_2CTA != 0;
   // X box: only as many token rows as the problem has (OOB rows would still cross the
   // crossbar as zero fill)
-  const int x_rows = pair ? p2::BT2 / 2 : std::min(BT, (M + 15) / 16 * 16);
+  const int x_rows = std::min(BT, (M + 15) / 16 * 16);
   bool ok = encode_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_UINT16, X, (uint64_t)K, (uint64_t)M,
                       (uint64_t)K * 2, BK, x_rows, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
@@ -1068,53 +666,32 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
     *why = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
-  const int num_tiles = pair ? ((N + 2 * BM - 1) / (2 * BM)) * ((M + p2::BT2 - 1) / p2::BT2)
-                            : ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int num_tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
   const bool sk = prefill_streamk(M, N, K);
   const int units = num_tiles * G;
-  const int grid = pair ? 2 * std::min(num_tiles, num_sms() / 2)
-                        : (sk ? std::min(units, num_sms()) : std::min(num_tiles, num_sms()));
+  const int grid = sk ? std::min(units, num_sms()) : std::min(num_tiles, num_sms());
   const int cta_q = units / grid, cta_r = units % grid;
   float* partials = reinterpret_cast<float*>(ws);
   int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
-  auto kern1 = x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>;
-  auto kern2 = x_dtype == SQ_BF16 ? prefill2_kernel<true> : prefill2_kernel<false>;
-  const int smem = pair ? p2::SMEM_ALLOC : SMEM_ALLOC;
-  cudaError_t e = pair ? cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-                       : cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = SMEM_ALLOC;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = option(SQ_OPT_PDL) ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = pair ? 2 : 1;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  const int early = option(SQ_OPT_PDL) && option(SQ_OPT_WEIGHTS_STATIC);
-  if (pair)
-    e = cudaLaunchKernelEx(&cfg, kern2, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early);
-  else
-    e = cudaLaunchKernelEx(&cfg, kern1, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early,
-                           x_rows * BK * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
+  cfg.numAttrs = 1;
+  const int early = option(SQ_OPT_PDL) && weights_static;
+  e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early,
+                         x_rows * BK * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 }  // namespace sq
 
-#if SQ_PRE_TRACE
-// development hook: copy the per-CTA wait-cycle trace of the last prefill launch
-extern "C" __attribute__((visibility("default"))) int sq_debug_prefill_trace(void* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, sq::g_pre_trace, sizeof(unsigned long long) * (size_t)n);
-}
-extern "C" __attribute__((visibility("default"))) int sq_debug_prefill_timeline(void* host) {
-  return (int)cudaMemcpyFromSymbol(host, sq::g_pre_ts, sizeof(long long) * 16 * 1024);
-}
-#endif

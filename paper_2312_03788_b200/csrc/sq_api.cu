@@ -48,21 +48,17 @@ int num_sms() {
 
 constexpr int kDecodeMaxM = 16;
 
-size_t ws_partials_bytes() {
-  return std::max({decode_partials_bytes(), decode_tc_partials_bytes(), prefill_partials_bytes()});
-}
+size_t ws_partials_bytes() { return std::max(decode_partials_bytes(), prefill_partials_bytes()); }
 
 static int g_opt_pdl = 1;
-static int g_opt_weights_static = 0;
 static int g_opt_decode_schedule = SQ_SCHED_AUTO;
-static int g_opt_decode_kernel = SQ_DECK_MMA_SYNC;
+static int g_opt_decode_grid_limit = 0;
 
 int option(int opt) {
   switch (opt) {
     case SQ_OPT_PDL: return g_opt_pdl;
-    case SQ_OPT_WEIGHTS_STATIC: return g_opt_weights_static;
     case SQ_OPT_DECODE_SCHEDULE: return g_opt_decode_schedule;
-    case SQ_OPT_DECODE_KERNEL: return g_opt_decode_kernel;
+    case SQ_OPT_DECODE_GRID_LIMIT: return g_opt_decode_grid_limit;
     default: return -1;
   }
 }
@@ -73,7 +69,7 @@ using namespace sq;
 
 extern "C" {
 
-int sq_version(void) { return 100; }
+int sq_version(void) { return 200; }
 
 const char* sq_status_string(sq_status st) {
   switch (st) {
@@ -95,16 +91,14 @@ int sq_decode_max_m(void) { return kDecodeMaxM; }
 sq_status sq_set_option(int opt, int value) {
   switch (opt) {
     case SQ_OPT_PDL: g_opt_pdl = value ? 1 : 0; return SQ_OK;
-    case SQ_OPT_WEIGHTS_STATIC: g_opt_weights_static = value ? 1 : 0; return SQ_OK;
     case SQ_OPT_DECODE_SCHEDULE:
       if (value < SQ_SCHED_AUTO || value > SQ_SCHED_ROWBLOCK)
         return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: decode schedule %d", value);
       g_opt_decode_schedule = value;
       return SQ_OK;
-    case SQ_OPT_DECODE_KERNEL:
-      if (value != SQ_DECK_MMA_SYNC && value != SQ_DECK_TCGEN05)
-        return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: decode kernel %d", value);
-      g_opt_decode_kernel = value;
+    case SQ_OPT_DECODE_GRID_LIMIT:
+      if (value < 0) return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: grid limit %d", value);
+      g_opt_decode_grid_limit = value;
       return SQ_OK;
     default: return fail(SQ_ERR_UNSUPPORTED, "sq_set_option: unknown option %d", opt);
   }
@@ -149,6 +143,26 @@ sq_status sq_smooth_scales(const void* W, int w_dtype, int64_t N, int64_t K, con
   return cuda_status(launch_smooth_finalize(act_max, s_out, K, alpha, eps, st), "smooth_finalize");
 }
 
+sq_status sq_smooth_scales_wmax(const float* w_max, const float* act_max, int64_t K, double alpha, double eps,
+                                float* s_out, void* stream) {
+  g_last_error.clear();
+  if (!w_max || !act_max || !s_out) return fail(SQ_ERR_NULL, "sq_smooth_scales_wmax: null pointer");
+  if (K <= 0) return fail(SQ_ERR_SHAPE, "sq_smooth_scales_wmax: K=%lld", (long long)K);
+  if (!(alpha >= 0.0 && alpha <= 1.0) || !(eps > 0.0))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_scales_wmax: alpha=%g eps=%g", alpha, eps);
+  if (!aligned16(w_max) || !aligned16(s_out) || !aligned16(act_max))
+    return fail(SQ_ERR_ALIGN, "sq_smooth_scales_wmax: unaligned pointer");
+  if ((const void*)act_max == (const void*)s_out)
+    return fail(SQ_ERR_UNSUPPORTED, "sq_smooth_scales_wmax: s_out aliases act_max");
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((const void*)w_max != (const void*)s_out) {
+    sq_status r = cuda_status(cudaMemcpyAsync(s_out, w_max, (size_t)K * sizeof(float), cudaMemcpyDeviceToDevice, st),
+                              "memcpy");
+    if (r != SQ_OK) return r;
+  }
+  return cuda_status(launch_smooth_finalize(act_max, s_out, K, alpha, eps, st), "smooth_finalize");
+}
+
 sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s, int64_t N,
                                      int64_t K, int group, uint8_t* Wq, uint16_t* scales,
                                      uint16_t* zeros, int* nonfinite_count, void* stream) {
@@ -172,21 +186,28 @@ size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group)
   return std::max(decode_workspace_bytes(N), prefill_workspace_bytes(M, N, K));
 }
 
-sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                             const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K,
-                             int group, void* workspace, size_t workspace_bytes, int path,
-                             void* stream) {
+sq_status sq_workspace_reset(void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error.clear();
+  if (workspace_bytes == 0) return SQ_OK;
+  if (!workspace) return fail(SQ_ERR_NULL, "sq_workspace_reset: null pointer");
+  return cuda_status(cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream), "sq_workspace_reset");
+}
+
+sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                           const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K, int group,
+                           void* workspace, size_t workspace_bytes, int path, unsigned flags, void* stream) {
   g_last_error.clear();
   if (M == 0 && N > 0 && K > 0) return SQ_OK;  // no-op; X/Y may be empty (null) tensors
   if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm: null pointer");
   if (M < 0 || N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
   if (group != 128 || K % group != 0 || !valid_dtype(x_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
+  if (flags & ~(unsigned)SQ_GEMM_WEIGHTS_STATIC) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: flags 0x%x", flags);
   if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
       !aligned16(Y))
     return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm: N %% 8 != 0 or unaligned pointer");
   if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: too large");
-  if (M == 0) return SQ_OK;
+  const bool wstatic = (flags & SQ_GEMM_WEIGHTS_STATIC) != 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (path == SQ_PATH_AUTO) path = (M <= kDecodeMaxM) ? SQ_PATH_DECODE : SQ_PATH_PREFILL;
   if (path == SQ_PATH_DECODE) {
@@ -195,9 +216,7 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
     if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: decode needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
-    cudaError_t e = g_opt_decode_kernel == SQ_DECK_TCGEN05
-                        ? launch_decode_tc(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why)
-                        : launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, st, &why);
+    cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, wstatic, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
     return cuda_status(e, "decode");
   }
@@ -207,18 +226,26 @@ sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, cons
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
     cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K,
-                                   workspace, workspace_bytes, st, &why);
+                                   workspace, workspace_bytes, wstatic, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm prefill: %s", why);
     return cuda_status(e, "prefill");
   }
   return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: unknown path %d", path);
 }
 
+sq_status sq_w4a16_gemm_path(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                             const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K,
+                             int group, void* workspace, size_t workspace_bytes, int path,
+                             void* stream) {
+  return sq_w4a16_gemm_ex(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace, workspace_bytes, path, 0u,
+                          stream);
+}
+
 sq_status sq_w4a16_gemm(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                         const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K, int group,
                         void* workspace, size_t workspace_bytes, void* stream) {
-  return sq_w4a16_gemm_path(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace,
-                            workspace_bytes, SQ_PATH_AUTO, stream);
+  return sq_w4a16_gemm_ex(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace, workspace_bytes,
+                          SQ_PATH_AUTO, 0u, stream);
 }
 
 sq_status sq_smooth_activations(const void* X, int x_dtype, const float* s, int64_t M, int64_t K,
@@ -266,8 +293,11 @@ sq_status sq_sq_diff_sum(const void* A, const void* B, int dtype, int64_t n, dou
 sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                                   const uint16_t* zeros, void* Y, int64_t M, int64_t N, int64_t K, int group,
                                   void* workspace, size_t workspace_bytes, void* const* peer_bufs, int rank,
-                                  int world, int64_t n_max, uint32_t epoch, int* error_flag, void* stream) {
+                                  int world, int64_t n_max, uint32_t epoch, int* error_flag, unsigned flags,
+                                  void* stream) {
   g_last_error.clear();
+  if (flags & ~(unsigned)SQ_GEMM_WEIGHTS_STATIC)
+    return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: flags 0x%x", flags);
   if (world <= 0 || rank < 0 || rank >= world || M < 0 || N <= 0 || M * N > n_max)
     return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm_allreduce: M=%lld N=%lld n_max=%lld rank=%d world=%d", (long long)M,
                 (long long)N, (long long)n_max, rank, world);
@@ -277,10 +307,10 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
   if (!peer_bufs || !error_flag) return fail(SQ_ERR_NULL, "sq_w4a16_gemm_allreduce: null pointer");
   if (!aligned16(peer_bufs) || n_max % 8 != 0)
     return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: unaligned peer array or n_max %% 8 != 0");
-  if (M > kDecodeMaxM || g_opt_decode_kernel != SQ_DECK_MMA_SYNC) {
-    // prefill-sized (or tcgen05 decode): the GEMM, then the one-shot exchange kernel (PDL)
-    sq_status st = sq_w4a16_gemm(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace, workspace_bytes,
-                                 stream);
+  if (M > kDecodeMaxM) {
+    // prefill-sized: the GEMM, then the one-shot exchange kernel (PDL)
+    sq_status st = sq_w4a16_gemm_ex(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, workspace, workspace_bytes,
+                                    SQ_PATH_AUTO, flags, stream);
     if (st != SQ_OK) return st;
     return sq_allreduce_oneshot(Y, x_dtype, Y, M * N, n_max, peer_bufs, rank, world, epoch, error_flag, stream);
   }
@@ -297,7 +327,7 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
   const ArParams ar{reinterpret_cast<uint8_t* const*>(peer_bufs), n_max, error_flag, rank, world, epoch};
   const char* why = nullptr;
   cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace,
-                                (cudaStream_t)stream, &why, &ar);
+                                (flags & SQ_GEMM_WEIGHTS_STATIC) != 0, (cudaStream_t)stream, &why, &ar);
   if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: %s", why);
   return cuda_status(e, "sq_w4a16_gemm_allreduce");
 }

@@ -24,10 +24,6 @@ cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t 
 // overlap another call's partials in a shared workspace.
 size_t decode_partials_bytes();
 size_t prefill_partials_bytes();
-size_t decode_tc_partials_bytes();
-cudaError_t launch_decode_tc(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                             const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
-                             cudaStream_t st, const char** why);
 size_t ws_partials_bytes();
 // Counter region after the partials: at least 64 KB (16384 row blocks / tiles), so one
 // workspace sized for any of the usual shapes serves them all.
@@ -45,20 +41,33 @@ struct ArParams {
   int rank, world;
   uint32_t epoch;  // 0: device-managed
 };
+// weights_static: the caller promised (SQ_GEMM_WEIGHTS_STATIC) that the weights are not
+// written by the preceding kernels, so with PDL the weight loads may start before the
+// previous kernel has finished.
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws,
+                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, bool weights_static,
                           cudaStream_t st, const char** why, const ArParams* ar = nullptr);
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                            const uint16_t* zeros, void* Y, int M, int N, int K,
-                           void* workspace, size_t ws_bytes, cudaStream_t st, const char** why);
+                           void* workspace, size_t ws_bytes, bool weights_static, cudaStream_t st,
+                           const char** why);
 
 int num_sms();
 int option(int opt);
 
-// one-shot all-reduce over peer memory (k_allreduce.cu)
+// one-shot all-reduce over peer memory (k_allreduce.cu).  Symmetric buffer layout:
+//   [header 128 B][flags: 2 parities x world x kArMaxChunks uint32][slots: 2 parities x world
+//    slots of n_max elements, each slot 4 * n_max bytes (fp16 partials use the first half,
+//    the fused decode path ships bf16 partials as fp32)]
 constexpr int kArMaxChunks = 8192;  // 2048 outputs per chunk: n <= 16 Mi outputs per call
+constexpr size_t kArHeaderBytes = 128;
+__host__ __device__ inline size_t ar_flags_offset() { return kArHeaderBytes; }
+__host__ __device__ inline size_t ar_slot_offset(int world, int par, int q, int64_t n_max) {
+  return kArHeaderBytes + (size_t)2 * world * kArMaxChunks * sizeof(uint32_t) +
+         ((size_t)par * world + q) * (size_t)n_max * 4;
+}
 int64_t ar_chunk_elems();
 size_t ar_buffer_bytes(int64_t n_max, int world);
 cudaError_t launch_oneshot_allreduce(const void* y_local, int dtype, void* y_out, int64_t n, int64_t n_max,

@@ -10,6 +10,9 @@ Names follow the C ABI (and the paper's notation):
   smooth_scales(W, act_max, alpha)     Eq. 6 smoothing factors s
   quantize_pack_groupwise(W, s)        Eq. 5 fold + Eq. 1 INT4 quantize/pack
   w4a16_gemm(X, Wq, scales, zeros)     Eq. 3 W4A16 linear layer
+
+Argument checks here (shape, dtype, device of caller-supplied outputs and vectors) only
+protect the C ABI from out-of-bounds pointers; they do no arithmetic.
 """
 
 from __future__ import annotations
@@ -21,14 +24,13 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# SQ_LIB overrides the in-tree library (development A/B of tuning variants only)
-LIB_PATH = os.environ.get("SQ_LIB") or os.path.join(_HERE, "_lib", "libsq.so")
+LIB_PATH = os.path.join(_HERE, "_lib", "libsq.so")
 
 SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
 SQ_F16, SQ_BF16 = 0, 1
 SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
-SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC, SQ_OPT_DECODE_SCHEDULE, SQ_OPT_DECODE_KERNEL = 1, 2, 3, 4
-SQ_DECK_MMA_SYNC, SQ_DECK_TCGEN05 = 0, 1
+SQ_OPT_PDL, SQ_OPT_DECODE_SCHEDULE, SQ_OPT_DECODE_GRID_LIMIT = 1, 3, 5
+SQ_GEMM_WEIGHTS_STATIC = 1
 SQ_SCHED_AUTO, SQ_SCHED_STREAMK, SQ_SCHED_ROWBLOCK = 0, 1, 2
 GROUP = 128
 
@@ -59,17 +61,20 @@ def _load():
         "sq_get_option": (i32, [i32]),
         "sq_act_absmax": (i32, [vp, i32, i64, i64, vp, i32, vp]),
         "sq_smooth_scales": (i32, [vp, i32, i64, i64, vp, f64, f64, vp, vp]),
+        "sq_smooth_scales_wmax": (i32, [vp, vp, i64, f64, f64, vp, vp]),
+        "sq_workspace_reset": (i32, [vp, sz, vp]),
         "sq_quantize_pack_groupwise": (i32, [vp, i32, vp, i64, i64, i32, vp, vp, vp, vp, vp]),
         "sq_w4a16_gemm_workspace_bytes": (sz, [i64, i64, i64, i32]),
         "sq_w4a16_gemm": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp]),
         "sq_w4a16_gemm_path": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]),
+        "sq_w4a16_gemm_ex": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, c.c_uint, vp]),
         "sq_smooth_activations": (i32, [vp, i32, vp, i64, i64, vp, vp]),
         "sq_sq_diff_sum_workspace_bytes": (sz, []),
         "sq_fold_rows": (i32, [vp, i32, vp, i64, i64, vp, vp]),
         "sq_sq_diff_sum": (i32, [vp, vp, i32, i64, vp, vp, sz, vp]),
         "sq_allreduce_buffer_bytes": (sz, [i64, i32]),
         "sq_w4a16_gemm_allreduce": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp, i32, i32, i64,
-                                          c.c_uint32, vp, vp]),
+                                          c.c_uint32, vp, c.c_uint, vp]),
         "sq_allreduce_oneshot": (i32, [vp, i32, vp, i64, i64, vp, i32, i32, c.c_uint32, vp, vp]),
         "sq_ipc_handle_bytes": (sz, []),
         "sq_ipc_get_handle": (i32, [vp, vp, c.POINTER(sz)]),
@@ -87,8 +92,8 @@ def _load():
 EXPORTED = (
     "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_set_option",
     "sq_get_option", "sq_act_absmax",
-    "sq_smooth_scales", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
-    "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
+    "sq_smooth_scales", "sq_smooth_scales_wmax", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
+    "sq_workspace_reset", "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_w4a16_gemm_ex", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
     "sq_sq_diff_sum", "sq_fold_rows", "sq_allreduce_buffer_bytes", "sq_w4a16_gemm_allreduce", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
     "sq_ipc_get_handle", "sq_ipc_open_handle", "sq_ipc_close",
 )
@@ -129,6 +134,23 @@ def _need_cuda(*ts):
             raise ValueError("libsq entry points take contiguous tensors")
 
 
+def _check_out(out, shape, dtype, device, what="out"):
+    """A caller-supplied output must match exactly: the C ABI cannot see tensor sizes."""
+    if out is None:
+        return
+    if tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != device:
+        raise ValueError(f"{what}: need shape {tuple(shape)} {dtype} on {device}, got "
+                         f"{tuple(out.shape)} {out.dtype} on {out.device}")
+
+
+def _check_vec(v, K, what):
+    """fp32[K] device vectors (s, act_max, w_max, d)."""
+    if v is None:
+        return
+    if v.dtype != torch.float32 or v.numel() != K:
+        raise ValueError(f"{what}: need float32[{K}], got {v.dtype}[{v.numel()}]")
+
+
 def version() -> int:
     return _load().sq_version()
 
@@ -138,8 +160,7 @@ def decode_max_m() -> int:
 
 
 def set_option(opt: int, value: int) -> None:
-    """Process-wide launch option (SQ_OPT_PDL, SQ_OPT_WEIGHTS_STATIC, SQ_OPT_DECODE_SCHEDULE;
-    include/libsq.h)."""
+    """Process-wide launch option (SQ_OPT_PDL, SQ_OPT_DECODE_SCHEDULE; include/libsq.h)."""
     _check(_load().sq_set_option(int(opt), int(value)))
 
 
@@ -150,8 +171,9 @@ def get_option(opt: int) -> int:
 def act_absmax(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
                stream=None) -> torch.Tensor:
     """act_max[k] = max_t |X[t][k]| (calibration statistic of Eq. 6)."""
-    _need_cuda(X)
+    _need_cuda(X, out)
     T, K = X.shape
+    _check_out(out, (K,), torch.float32, X.device)
     if out is None:
         out = torch.empty(K, dtype=torch.float32, device=X.device)
     _check(_load().sq_act_absmax(_ptr(X), _dtype_code(X), T, K, _ptr(out), int(accumulate), _stream(stream)))
@@ -161,8 +183,10 @@ def act_absmax(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: boo
 def smooth_scales(W: torch.Tensor, act_max: torch.Tensor, alpha: float, eps: float = 1e-5,
                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Eq. 6 smoothing factors s[K] for the (possibly stacked) consumer weight W[N][K]."""
-    _need_cuda(W, act_max)
+    _need_cuda(W, act_max, out)
     N, K = W.shape
+    _check_vec(act_max, K, "act_max")
+    _check_out(out, (K,), torch.float32, W.device)
     if out is None:
         out = torch.empty(K, dtype=torch.float32, device=W.device)
     _check(_load().sq_smooth_scales(_ptr(W), _dtype_code(W), N, K, _ptr(act_max), float(alpha),
@@ -170,15 +194,52 @@ def smooth_scales(W: torch.Tensor, act_max: torch.Tensor, alpha: float, eps: flo
     return out
 
 
+def weight_absmax(W: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """w_max[k] = max_n |W[n][k]| (Eq. 6's weight maxima) -- the column abs-max kernel of
+    sq_act_absmax applied to the [N][K] weight."""
+    return act_absmax(W, out=out, stream=stream)
+
+
+def smooth_scales_wmax(w_max: torch.Tensor, act_max: torch.Tensor, alpha: float, eps: float = 1e-5,
+                       out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Eq. 6 from precomputed maxima (sq_smooth_scales_wmax): used by tensor-parallel
+    shards after a MAX all-reduce of w_max, so every rank folds the same s."""
+    _need_cuda(w_max, act_max, out)
+    K = w_max.numel()
+    _check_vec(w_max, K, "w_max")
+    _check_vec(act_max, K, "act_max")
+    _check_out(out, (K,), torch.float32, w_max.device)
+    if out is None:
+        out = torch.empty(K, dtype=torch.float32, device=w_max.device)
+    _check(_load().sq_smooth_scales_wmax(_ptr(w_max), _ptr(act_max), K, float(alpha), float(eps), _ptr(out),
+                                         _stream(stream)))
+    return out
+
+
 @dataclass
 class QuantizedLinear:
-    """W4 g128 weight: codes [N][K/2] u8, scales/zeros [G][N] fp16 bits (as int16 tensors)."""
+    """W4 g128 weight: codes [N][K/2] u8, scales/zeros [G][N] fp16 bits (as int16 tensors).
+
+    static: the weights are final (inference).  GEMMs on this handle then pass
+    SQ_GEMM_WEIGHTS_STATIC, letting the kernel stream its first weight stages before the
+    previous kernel on the stream has finished.  A freshly quantized handle is not static
+    until the caller says so (mark_static), because the quantize kernel that wrote it may
+    still be running."""
     Wq: torch.Tensor
     scales: torch.Tensor
     zeros: torch.Tensor
     N: int
     K: int
     group: int = GROUP
+    static: bool = False
+
+    def mark_static(self, static: bool = True) -> "QuantizedLinear":
+        self.static = static
+        return self
+
+    @property
+    def flags(self) -> int:
+        return SQ_GEMM_WEIGHTS_STATIC if self.static else 0
 
     def nbytes(self) -> int:
         return self.Wq.numel() + 2 * self.scales.numel() + 2 * self.zeros.numel()
@@ -190,6 +251,9 @@ def quantize_pack_groupwise(W: torch.Tensor, s: torch.Tensor | None = None, grou
     _need_cuda(W, s, nonfinite)
     N, K = W.shape
     dev = W.device
+    _check_vec(s, K, "s")
+    if nonfinite is not None and (nonfinite.dtype != torch.int32 or nonfinite.numel() < 1):
+        raise ValueError("nonfinite: need an int32 device counter")
     Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=dev)
     scales = torch.empty((K // group, N), dtype=torch.int16, device=dev)
     zeros = torch.empty((K // group, N), dtype=torch.int16, device=dev)
@@ -200,6 +264,12 @@ def quantize_pack_groupwise(W: torch.Tensor, s: torch.Tensor | None = None, grou
 
 def w4a16_gemm_workspace_bytes(M: int, N: int, K: int, group: int = GROUP) -> int:
     return int(_load().sq_w4a16_gemm_workspace_bytes(M, N, K, group))
+
+
+def workspace_reset(ws: torch.Tensor, stream=None) -> None:
+    """Zero a GEMM workspace or all-reduce buffer on the stream (sq_workspace_reset)."""
+    _need_cuda(ws)
+    _check(_load().sq_workspace_reset(_ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 _WS: dict = {}
@@ -224,6 +294,7 @@ def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = N
     M, K = X.shape
     if K != q.K:
         raise ValueError(f"K mismatch: X has {K}, weight has {q.K}")
+    _check_out(out, (M, q.N), X.dtype, X.device)
     if out is None:
         out = torch.empty((M, q.N), dtype=X.dtype, device=X.device)
     if workspace is None:
@@ -231,17 +302,19 @@ def w4a16_gemm(X: torch.Tensor, q: QuantizedLinear, out: torch.Tensor | None = N
         if need:
             workspace = default_workspace(X.device, need)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(_load().sq_w4a16_gemm_path(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
-                                      _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes, int(path),
-                                      _stream(stream)))
+    _check(_load().sq_w4a16_gemm_ex(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
+                                    _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes, int(path),
+                                    q.flags, _stream(stream)))
     return out
 
 
 def smooth_activations(X: torch.Tensor, s: torch.Tensor, out: torch.Tensor | None = None,
                        stream=None) -> torch.Tensor:
     """X̂ = RN(X / s) per input channel (activation side of Eq. 5); out may be X (in place)."""
-    _need_cuda(X, s)
+    _need_cuda(X, s, out)
     M, K = X.shape
+    _check_vec(s, K, "s")
+    _check_out(out, (M, K), X.dtype, X.device)
     if out is None:
         out = torch.empty_like(X)
     _check(_load().sq_smooth_activations(_ptr(X), _dtype_code(X), _ptr(s), M, K, _ptr(out), _stream(stream)))
@@ -276,7 +349,10 @@ def allreduce_oneshot(y_local: torch.Tensor, peers_dev: torch.Tensor, rank: int,
     """One-shot all-reduce of the row-parallel partial y_local over peer memory
     (include/libsq.h sq_allreduce_oneshot).  peers_dev: int64 device tensor of the world
     symmetric-buffer addresses as mapped in this process."""
-    _need_cuda(y_local, peers_dev, error_flag)
+    _need_cuda(y_local, peers_dev, error_flag, out)
+    _check_out(out, tuple(y_local.shape), y_local.dtype, y_local.device)
+    if y_local.numel() > n_max:
+        raise ValueError(f"allreduce: {y_local.numel()} elements > n_max {n_max}")
     if out is None:
         out = y_local
     _check(_load().sq_allreduce_oneshot(_ptr(y_local), _dtype_code(y_local), _ptr(out), y_local.numel(),
@@ -315,6 +391,7 @@ def w4a16_gemm_allreduce(X: torch.Tensor, q: QuantizedLinear, peers_dev: torch.T
     M, K = X.shape
     if K != q.K:
         raise ValueError(f"K mismatch: X has {K}, weight has {q.K}")
+    _check_out(out, (M, q.N), X.dtype, X.device)
     if out is None:
         out = torch.empty((M, q.N), dtype=X.dtype, device=X.device)
     if workspace is None:
@@ -325,15 +402,18 @@ def w4a16_gemm_allreduce(X: torch.Tensor, q: QuantizedLinear, peers_dev: torch.T
     _check(_load().sq_w4a16_gemm_allreduce(_ptr(X), _dtype_code(X), _ptr(q.Wq), _ptr(q.scales), _ptr(q.zeros),
                                            _ptr(out), M, q.N, K, q.group, _ptr(workspace), ws_bytes,
                                            _ptr(peers_dev), int(rank), int(world), int(n_max),
-                                           ctypes.c_uint32(epoch & 0xFFFFFFFF), _ptr(error_flag), _stream(stream)))
+                                           ctypes.c_uint32(epoch & 0xFFFFFFFF), _ptr(error_flag), q.flags,
+                                           _stream(stream)))
     return out
 
 
 def fold_rows(W: torch.Tensor, d: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """W_out[n][k] = RN(W[n][k] / d[n]): fold the consumer's smoothing factors into the
     producer linear's output rows (Fig. 5); out may be W (in place)."""
-    _need_cuda(W, d)
+    _need_cuda(W, d, out)
     N, K = W.shape
+    _check_vec(d, N, "d")
+    _check_out(out, (N, K), W.dtype, W.device)
     if out is None:
         out = torch.empty_like(W)
     _check(_load().sq_fold_rows(_ptr(W), _dtype_code(W), _ptr(d), N, K, _ptr(out), _stream(stream)))

@@ -59,8 +59,15 @@ def synth_act_max(K: int, seed: int, device) -> torch.Tensor:
 def build_stack(model: ModelShape = CODELLAMA_34B, layers: int | None = None, rank: int = 0,
                 world: int = 1, device="cuda", seed: int = 1234, smooth: bool = True,
                 group=None) -> LinearStack:
-    """Quantize `layers` decoder layers' linears for this rank.  Each rank draws only its
-    own shard; smoothing factors are computed on the shard (setup only, not timed)."""
+    """Quantize `layers` decoder layers' linears for this rank (setup, not timed).  Each
+    rank draws only its own shard.  Eq. 6's weight maxima are those of the FULL weight: a
+    column-parallel shard holds some output rows of every input channel, so the ranks
+    all-reduce their shard's column maxima with MAX before computing s (every rank folds
+    the same s, as a real tensor-parallel deployment of Eq. 5/6 would); a row-parallel
+    shard holds whole input channels, so its maxima are already complete.  The returned
+    weights are resident and final, so their GEMMs run with SQ_GEMM_WEIGHTS_STATIC."""
+    import torch.distributed as dist
+
     L = model.layers if layers is None else layers
     st = LinearStack(model, rank, world, group=group)
     shards = layer_shards(model, rank, world)
@@ -71,10 +78,17 @@ def build_stack(model: ModelShape = CODELLAMA_34B, layers: int | None = None, ra
             s = None
             if smooth:
                 am = synth_act_max(sh.K, seed + 7 * si, device)
-                s = sq.smooth_scales(W, am, 0.5)
+                w_max = sq.weight_absmax(W)
+                if group is not None and world > 1 and sh.kind == "col":
+                    dist.all_reduce(w_max, op=dist.ReduceOp.MAX, group=group)
+                s = sq.smooth_scales_wmax(w_max, am, 0.5)
             row.append(Linear(sh, sq.quantize_pack_groupwise(W, s)))
             del W
         st.layers.append(row)
+    torch.cuda.synchronize(device)  # the quantize kernels are done: the weights are final
+    for row in st.layers:
+        for lin in row:
+            lin.q.mark_static()
     return st
 
 
@@ -114,7 +128,13 @@ def run_pass(st: LinearStack, buf: PassBuffers, path: int = sq.SQ_PATH_AUTO, wor
             sq.w4a16_gemm(buf.x[lin.shard.name], lin.q, out=y, path=path, workspace=workspace)
             n += 1
             if lin.shard.allreduce and st.group is not None:
-                dist.all_reduce(y, group=st.group)
+                if y.dtype == torch.bfloat16:
+                    # reduce bf16 partials in fp32, round once
+                    y32 = y.float()
+                    dist.all_reduce(y32, group=st.group)
+                    y.copy_(y32)
+                else:
+                    dist.all_reduce(y, group=st.group)
     return n
 
 

@@ -82,3 +82,42 @@ def quantize_group(values, n_bits: int = 4):
     Z = min(max(rha(-lo / d), 0), qmax)
     codes = [min(max(rha(v / d) + Z, 0), qmax) for v in F]
     return codes, d, Z
+
+
+# bfloat16: 8-bit significand (7 stored bits), fp32's exponent range (emin = -126,
+# subnormal quantum 2^-133), largest finite (2 - 2^-7) * 2^127.
+BF16_MAX = (2 - Fraction(1, 2 ** 7)) * Fraction(2) ** 127
+BF16_QUANTUM_MIN = Fraction(1, 2 ** 133)
+
+
+def _quantum_bf16(a: Fraction) -> Fraction:
+    """Spacing of bf16 values in the binade containing a > 0."""
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    elif Fraction(2) ** (e + 1) <= a:
+        e += 1
+    if e < -126:
+        return BF16_QUANTUM_MIN
+    return Fraction(2) ** (e - 7)
+
+
+def rn_bf16(x: Fraction):
+    """Exact round-to-nearest-even to bf16; returns the value, or None on overflow
+    (|x| at or above the midpoint between BF16_MAX and 2^128 rounds to Inf)."""
+    if x == 0:
+        return Fraction(0)
+    s = 1 if x > 0 else -1
+    a = abs(x)
+    q = _quantum_bf16(a)
+    lo = (a // q) * q
+    rem = a - lo
+    if rem * 2 > q:
+        r = lo + q
+    elif rem * 2 < q:
+        r = lo
+    else:
+        r = lo if ((lo / q) % 2 == 0) else lo + q
+    if r > BF16_MAX:
+        return None
+    return s * r

@@ -142,7 +142,7 @@ def test_allreduce_argument_errors(L):
     assert call(err=None) == sq.SQ_ERR_NULL
     assert call(n_max=1028, n=1028) == sq.SQ_ERR_ALIGN
     assert call(n=0) == sq.SQ_OK
-    assert L.sq_allreduce_buffer_bytes(1024, 2) >= 2 * 2 * 1024 * 2
+    assert L.sq_allreduce_buffer_bytes(1024, 2) >= 2 * 2 * 1024 * 4   # 4-byte slot stride
     assert L.sq_ipc_handle_bytes() == 64
     assert L.sq_ipc_get_handle(None, FAKE, None) == sq.SQ_ERR_NULL
     assert L.sq_ipc_open_handle(None, None) == sq.SQ_ERR_NULL
@@ -153,8 +153,9 @@ def test_gemm_allreduce_argument_errors(L):
     """sq_w4a16_gemm_allreduce validates on the host before any launch."""
     f = L.sq_w4a16_gemm_allreduce
 
-    def call(M=4, N=256, K=512, rank=0, world=2, n_max=1024, peers=FAKE, err=FAKE, dt=0, g=128):
-        return f(FAKE, dt, FAKE, FAKE, FAKE, FAKE, M, N, K, g, FAKE, 1 << 20, peers, rank, world, n_max, 0, err, None)
+    def call(M=4, N=256, K=512, rank=0, world=2, n_max=1024, peers=FAKE, err=FAKE, dt=0, g=128, flags=0):
+        return f(FAKE, dt, FAKE, FAKE, FAKE, FAKE, M, N, K, g, FAKE, 1 << 20, peers, rank, world, n_max, 0, err,
+                 flags, None)
 
     assert call(n_max=512) == sq.SQ_ERR_SHAPE       # M*N > n_max
     assert call(rank=2) == sq.SQ_ERR_SHAPE
@@ -163,7 +164,28 @@ def test_gemm_allreduce_argument_errors(L):
     assert call(err=None) == sq.SQ_ERR_NULL
     assert call(n_max=1028) == sq.SQ_ERR_ALIGN
     assert call(g=64) == sq.SQ_ERR_UNSUPPORTED
+    assert call(flags=2) == sq.SQ_ERR_UNSUPPORTED   # unknown flag bit
     assert call(M=0) == sq.SQ_OK
+
+
+def test_gemm_ex_flags_and_options(L):
+    """Per-call flags (SQ_GEMM_WEIGHTS_STATIC) replace the version-1 process-wide option 2."""
+    f = L.sq_w4a16_gemm_ex
+    args = (FAKE, 0, FAKE, FAKE, FAKE, FAKE, 0, 256, 512, 128, None, 0, 0)
+    assert f(*args, sq.SQ_GEMM_WEIGHTS_STATIC, None) == sq.SQ_OK      # M = 0: no-op
+    assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 256, 512, 128, None, 0, 0, 4, None) == sq.SQ_ERR_UNSUPPORTED
+    assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 256, 512, 128, None, 0, 1, 1, None) == sq.SQ_ERR_WORKSPACE
+    assert L.sq_set_option(2, 1) == sq.SQ_ERR_UNSUPPORTED            # removed process-wide switch
+    assert L.sq_set_option(4, 1) == sq.SQ_ERR_UNSUPPORTED            # removed tcgen05-decode switch
+    assert L.sq_get_option(sq.SQ_OPT_PDL) in (0, 1)
+    assert L.sq_workspace_reset(None, 0, None) == sq.SQ_OK
+    assert L.sq_workspace_reset(None, 16, None) == sq.SQ_ERR_NULL
+    w = L.sq_smooth_scales_wmax
+    assert w(None, FAKE, 128, 0.5, 1e-5, FAKE, None) == sq.SQ_ERR_NULL
+    assert w(FAKE, FAKE, 0, 0.5, 1e-5, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_SHAPE
+    assert w(FAKE, FAKE, 128, -0.5, 1e-5, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_UNSUPPORTED
+    assert w(FAKE, FAKE, 128, 0.5, 1e-5, FAKE, None) == sq.SQ_ERR_UNSUPPORTED   # s_out aliases act_max
+    assert w(FAKE_MIS, FAKE, 128, 0.5, 1e-5, ctypes.c_void_p(1 << 21), None) == sq.SQ_ERR_ALIGN
 
 
 def test_fold_rows_argument_errors(L):

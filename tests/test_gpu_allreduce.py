@@ -82,15 +82,23 @@ def test_oneshot_in_place_and_timeout():
 @pytest.mark.parametrize("N,K", [(1024, 1024), (2048, 2048), (1024, 3072)])
 def test_fused_gemm_allreduce_streams(M, N, K, dtype):
     """sq_w4a16_gemm_allreduce (decode: one kernel) for two ranks on two streams of one GPU
-    (grids of <= 148 CTAs, so both kernels are resident together): every rank's Y equals the
-    rank-ordered fp32 sum of the two ranks' plain sq_w4a16_gemm partials, bit for bit, over
-    back-to-back calls (both epoch parities, device-managed epoch)."""
+    (grids of <= 148 CTAs, so both kernels are resident together), over back-to-back calls
+    (both epoch parities, device-managed epoch).  Every rank gets the bit-identical Y, equal
+    to the unsharded fp64 oracle within the dtype bound and the element-wise bound (the
+    fused call cuts N from N alone, so its fp32 partials may be summed in another order
+    than a plain sq_w4a16_gemm of the same shard; fp16 partials travel as fp16, bf16 ones as
+    fp32)."""
+    import oracle
     from paper_2312_03788_b200 import synth, tp
+    from tests.gemm_bounds import elementwise_ratio
 
     world = 2
-    W = torch.from_numpy(synth.weights(N, K, seed=N + K)).to(DEV)
+    W_np = synth.weights(N, K, seed=N + K)
+    W = torch.from_numpy(W_np).to(DEV)
     ranges = tp.channel_split(K, world)
     qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()) for a, b in ranges]
+    full = oracle.quantize_pack(W_np, None)
+    W_hat = oracle.dequant(full["Wq"], full["scales"], full["zeros"])
     n_max = M * N
     nb = sq.allreduce_buffer_bytes(n_max, world)
     bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
@@ -102,7 +110,6 @@ def test_fused_gemm_allreduce_streams(M, N, K, dtype):
     for it in range(4):
         X = (torch.randn(M, K, generator=g, device=DEV) * 2).to(dtype)
         xs = [X[:, a:b].contiguous() for a, b in ranges]
-        parts = [sq.w4a16_gemm(xs[r], qs[r]) for r in range(world)]
         outs = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)]
         torch.cuda.synchronize()
         for r in range(world):
@@ -111,9 +118,134 @@ def test_fused_gemm_allreduce_streams(M, N, K, dtype):
                                         workspace=wss[r], stream=streams[r])
         torch.cuda.synchronize()
         assert all(int(e.item()) == 0 for e in errs)
-        want = _expected(parts)
+        assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), it
+        xd = "f16" if dtype == torch.float16 else "bf16"
+        x64 = X.float().cpu().double().numpy()
+        y_ref = x64 @ W_hat.T
+        y = outs[0].float().cpu().double().numpy()
+        assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= (1e-3 if xd == "f16" else 4e-3)
+        assert elementwise_ratio(y, y_ref, x64, W_hat, xd) <= 1.0
+
+
+@pytest.fixture
+def grid_limit():
+    """Cap decode grids so that P simulated ranks' fused kernels are co-resident on one GPU."""
+    def set_limit(v):
+        sq.set_option(sq.SQ_OPT_DECODE_GRID_LIMIT, v)
+    yield set_limit
+    sq.set_option(sq.SQ_OPT_DECODE_GRID_LIMIT, 0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("layer", ["o_proj", "down"])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_fused_allreduce_34b_tp_shards(P, layer, dtype, grid_limit):
+    """The fused row-parallel GEMM + all-reduce at the Code Llama-34B tensor-parallel shard
+    shapes: o_proj K_r = 8192 / P, down_proj K_r from the group-aligned
+    split of 172 groups (P = 8: 22,22,22,22,21,21,21,21 -> K_r = 2816 / 2688, a rank-dependent
+    ragged final stage).  All P ranks run as concurrent kernels on P streams (grids capped
+    so they are co-resident), M in {1, 16}, device-managed epochs, against the unsharded
+    fp64 oracle on sampled output rows; every rank holds the bit-identical Y."""
+    import oracle
+    from paper_2312_03788_b200 import stack, tp
+    from tests.gemm_bounds import elementwise_ratio
+
+    K, N = (8192, 8192) if layer == "o_proj" else (22016, 8192)
+    W = stack.synth_weight(N, K, 41 + P, DEV)
+    ranges = tp.channel_split(K, P)
+    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()).mark_static() for a, b in ranges]
+    rows = np.sort(np.random.default_rng(P).choice(N, 48, replace=False))
+    ref = oracle.quantize_pack(W[rows].cpu().numpy(), None)      # rows quantize independently (P14)
+    W_hat = oracle.dequant(ref["Wq"], ref["scales"], ref["zeros"])
+    torch.cuda.synchronize()
+    n_max = 16 * N
+    nb = sq.allreduce_buffer_bytes(n_max, P)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(P)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    errs = [torch.zeros(1, dtype=torch.int32, device=DEV) for _ in range(P)]
+    wss = [torch.zeros(sq.w4a16_gemm_workspace_bytes(16, N, b - a), dtype=torch.uint8, device=DEV)
+           for a, b in ranges]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    grid_limit(max(1, 2 * torch.cuda.get_device_properties(0).multi_processor_count // P - 2))
+    g = torch.Generator(device=DEV).manual_seed(P * 3 + K)
+    for M in (1, 16, 1):
+        X = torch.randn(M, K, generator=g, device=DEV).to(dtype)
+        xs = [X[:, a:b].contiguous() for a, b in ranges]
+        outs = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(P)]
+        torch.cuda.synchronize()
+        for r in range(P):
+            with torch.cuda.stream(streams[r]):
+                sq.w4a16_gemm_allreduce(xs[r], qs[r], peers, r, P, n_max, errs[r], out=outs[r],
+                                        workspace=wss[r], stream=streams[r])
+        torch.cuda.synchronize()
+        assert all(int(e.item()) == 0 for e in errs), [int(e.item()) for e in errs]
+        for r in range(1, P):
+            assert torch.equal(outs[0].view(torch.int16), outs[r].view(torch.int16)), (M, r)
+        x64 = X.float().cpu().double().numpy()
+        y_ref = x64 @ W_hat.T
+        y = outs[0].float().cpu().double().numpy()[:, rows]
+        xd = "f16" if dtype == torch.float16 else "bf16"
+        assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= (1e-3 if xd == "f16" else 4e-3), M
+        assert elementwise_ratio(y, y_ref, x64, W_hat, xd) <= 1.0, M
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_fused_allreduce_back_to_back_pdl(dtype):
+    """Several fused calls on one stream per rank with NO host synchronization in between,
+    programmatic dependent launch on, device-managed epochs (epoch 0), interleaved with
+    plain GEMMs on the same streams (the epoch must be read only after the
+    previous call's grid completed).  Every call's result is checked afterwards."""
+    from paper_2312_03788_b200 import synth, tp
+
+    world, M, N, K = 2, 4, 1024, 2048
+    W = torch.from_numpy(synth.weights(N, K, seed=5)).to(DEV)
+    ranges = tp.channel_split(K, world)
+    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()).mark_static() for a, b in ranges]
+    q_plain = sq.quantize_pack_groupwise(W[:, :1024].contiguous()).mark_static()
+    n_max = M * N
+    nb = sq.allreduce_buffer_bytes(n_max, world)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    errs = [torch.zeros(1, dtype=torch.int32, device=DEV) for _ in range(world)]
+    wss = [torch.zeros(sq.w4a16_gemm_workspace_bytes(M, N, K), dtype=torch.uint8, device=DEV) for _ in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    g = torch.Generator(device=DEV).manual_seed(11)
+    calls = 8
+    Xs = [(torch.randn(M, K, generator=g, device=DEV)).to(dtype) for _ in range(calls)]
+    outs = [[torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)] for _ in range(calls)]
+    plain = [[None] * world for _ in range(calls)]
+    old = sq.get_option(sq.SQ_OPT_PDL)
+    sq.set_option(sq.SQ_OPT_PDL, 1)
+    try:
+        torch.cuda.synchronize()
         for r in range(world):
-            assert torch.equal(outs[r].view(torch.int16), want.view(torch.int16)), (it, r)
+            with torch.cuda.stream(streams[r]):
+                for c in range(calls):
+                    a, b = ranges[r]
+                    sq.w4a16_gemm_allreduce(Xs[c][:, a:b].contiguous(), qs[r], peers, r, world, n_max, errs[r],
+                                            out=outs[c][r], workspace=wss[r], stream=streams[r])
+                    if c % 3 == 1:  # a plain decode GEMM between two fused calls
+                        plain[c][r] = sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), q_plain, workspace=wss[r],
+                                                    stream=streams[r])
+        torch.cuda.synchronize()
+    finally:
+        sq.set_option(sq.SQ_OPT_PDL, old)
+    assert all(int(e.item()) == 0 for e in errs)
+    for c in range(calls):
+        # the same call again, isolated (synchronized before and after): deterministic
+        ref = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)]
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                a, b = ranges[r]
+                sq.w4a16_gemm_allreduce(Xs[c][:, a:b].contiguous(), qs[r], peers, r, world, n_max, errs[r],
+                                        out=ref[r], workspace=wss[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert torch.equal(outs[c][r].view(torch.int16), outs[c][0].view(torch.int16)), (c, r)
+            assert torch.equal(outs[c][r].view(torch.int16), ref[r].view(torch.int16)), (c, r)
+            if plain[c][r] is not None:
+                assert torch.equal(plain[c][r], sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), q_plain)), (c, r)
+    assert all(int(e.item()) == 0 for e in errs)
 
 
 def _free_port():

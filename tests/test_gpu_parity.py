@@ -6,7 +6,9 @@ same seeded inputs.
     rounded on either side).
   * GEMM: relative Frobenius error <= 5e-3 (BASELINE.json north_star), fp32
     accumulate; the expected error from rounding Ŵ/Y is ~3e-4 (fp16) / ~2.4e-3
-    (bf16), so the test also checks a tighter dtype-specific bound.
+    (bf16), so the test also checks a tighter dtype-specific bound, AND every output
+    element against the floating-point bound of tests/gemm_bounds.py (a wrong row block
+    or tail tile cannot hide under the norm).
 """
 
 from __future__ import annotations
@@ -17,6 +19,7 @@ import torch
 
 import oracle
 from paper_2312_03788_b200 import sq, synth
+from tests.gemm_bounds import elementwise_ratio
 
 pytestmark = pytest.mark.gpu
 
@@ -140,15 +143,32 @@ def test_quantize_bf16_weights_bitexact():
 
 
 # ------------------------------------------------------------------ a6/a7 GEMM
-def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True):
-    W = synth.weights(N, K, seed=seed + 100, heavy=True)
+class GemmCase:
+    """GPU output and the oracle's exact result of one GEMM, plus what the element-wise
+    bound needs (the activations as fed, the exact dequantized weights)."""
+
+    def __init__(self, y, y_ref, x64, W_hat, xd):
+        self.y, self.y_ref, self.x64, self.W_hat, self.xd = y, y_ref, x64, W_hat, xd
+
+    def check(self, dtype, frob=None):
+        err = _rel_frob(self.y, self.y_ref)
+        assert err <= TOL_FROB and err <= (TIGHT[dtype] if frob is None else frob), err
+        ratio = elementwise_ratio(self.y.float().cpu().double().numpy(), self.y_ref, self.x64, self.W_hat,
+                                  self.xd)
+        assert ratio <= 1.0, ratio
+        return err
+
+
+def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0):
+    if W is None:
+        W = synth.weights(N, K, seed=seed + 100, heavy=True)
     s = None
     if smooth:
         am = oracle.act_absmax(synth.activations(2048, K, seed=seed + 200).astype(np.float16))
         s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
     ref_q = oracle.quantize_pack(W, s, 128)
     q = sq.quantize_pack_groupwise(_t(W), None if s is None else _t(s))
-    X = synth.activations(M, K, seed=seed + 300, outlier_seed=seed + 200)
+    X = synth.activations(M, K, seed=seed + 300, outlier_seed=seed + 200) * x_scale
     if s is not None:  # a5: X̂ = X diag(s)^-1, rounded once to the activation dtype
         X = X.astype(np.float64) / s.astype(np.float64)[None, :]
     x = torch.from_numpy(np.ascontiguousarray(X)).to(dtype).to(DEV)
@@ -160,32 +180,29 @@ def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True):
     torch.cuda.synchronize()
     xn, xd = _x_np_for(x)
     y_ref = oracle.gemm(xn, ref_q["Wq"], ref_q["scales"], ref_q["zeros"], 128, xd)
-    return y, y_ref
+    W_hat = oracle.dequant(ref_q["Wq"], ref_q["scales"], ref_q["zeros"], 128)
+    x64 = x.float().cpu().double().numpy()
+    return GemmCase(y, y_ref, x64, W_hat, xd)
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("M", [1, 2, 3, 4, 7, 8, 9, 13, 16])
 @pytest.mark.parametrize("N,K", [(512, 512), (264, 1152), (2048, 4096)])
 def test_gemm_decode_parity(M, N, K, dtype):
-    y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_DECODE, seed=M)
-    err = _rel_frob(y, y_ref)
-    assert err <= TOL_FROB and err <= TIGHT[dtype], err
+    _gemm_case(M, N, K, dtype, sq.SQ_PATH_DECODE, seed=M).check(dtype)
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("M", [17, 64, 256, 300, 520])
 @pytest.mark.parametrize("N,K", [(256, 512), (392, 1152), (1024, 2048)])
 def test_gemm_prefill_parity(M, N, K, dtype):
-    y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M)
-    err = _rel_frob(y, y_ref)
-    assert err <= TOL_FROB and err <= TIGHT[dtype], err
+    _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M).check(dtype)
 
 
 @pytest.mark.parametrize("M", [1, 16, 32])
 def test_gemm_prefill_small_m(M):
     """The prefill path is legal for any M (the M sweep maps both paths)."""
-    y, y_ref = _gemm_case(M, 384, 1024, torch.float16, sq.SQ_PATH_PREFILL, seed=7)
-    assert _rel_frob(y, y_ref) <= TIGHT[torch.float16]
+    _gemm_case(M, 384, 1024, torch.float16, sq.SQ_PATH_PREFILL, seed=7).check(torch.float16)
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
@@ -218,8 +235,7 @@ def test_gemm_auto_threshold():
     """SQ_PATH_AUTO: M <= M_dec runs decode, larger M prefill -- both correct."""
     assert sq.decode_max_m() == 16
     for M in (16, 17):
-        y, y_ref = _gemm_case(M, 256, 512, torch.float16, sq.SQ_PATH_AUTO, seed=M)
-        assert _rel_frob(y, y_ref) <= TIGHT[torch.float16]
+        _gemm_case(M, 256, 512, torch.float16, sq.SQ_PATH_AUTO, seed=M).check(torch.float16)
 
 
 def test_gemm_m_zero_noop():
@@ -230,35 +246,38 @@ def test_gemm_m_zero_noop():
 
 
 @pytest.mark.parametrize("pdl,static", [(0, 0), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M", [1, 16])
+@pytest.mark.parametrize("M", [1, 16, 40])
 def test_gemm_chain_launch_options(pdl, static, M):
-    """A dependent chain y_{i+1} = y_i · Ŵ_i^T (each GEMM reads the previous one's
-    output) under programmatic dependent launch and early weight streaming: the
-    kernels must still wait for their inputs (include/libsq.h SQ_OPT_*)."""
+    """A dependent chain y_{i+1} = y_i · Ŵ_i^T (each GEMM reads the previous one's output,
+    no host sync in between) under programmatic dependent launch and early weight
+    streaming (SQ_GEMM_WEIGHTS_STATIC on the handle): every kernel must still wait for its
+    input.  Each link is checked against the oracle applied to the GPU's own input of that
+    link, so a GEMM that read a stale X cannot pass; all links obey the 5e-3 contract and
+    the element-wise bound."""
     D = 512
     Ws = [synth.weights(D, D, seed=300 + i) for i in range(4)]
     refs = [oracle.quantize_pack(W, None) for W in Ws]
     qs = [sq.quantize_pack_groupwise(_t(W)) for W in Ws]
-    torch.cuda.synchronize()  # weights static before the chain (SQ_OPT_WEIGHTS_STATIC contract)
+    torch.cuda.synchronize()  # the quantize kernels finished: the weights are static now
+    for q in qs:
+        q.mark_static(bool(static))
     X = (synth.activations(M, D, seed=9) * 0.05).astype(np.float16)
-    old = (sq.get_option(sq.SQ_OPT_PDL), sq.get_option(sq.SQ_OPT_WEIGHTS_STATIC))
+    old = sq.get_option(sq.SQ_OPT_PDL)
+    ys = [torch.from_numpy(X).to(DEV)]
     try:
         sq.set_option(sq.SQ_OPT_PDL, pdl)
-        sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, static)
-        y = torch.from_numpy(X).to(DEV)
         for _ in range(3):
             for q in qs:
-                y = sq.w4a16_gemm(y, q, path=sq.SQ_PATH_DECODE)
+                ys.append(sq.w4a16_gemm(ys[-1], q))
         torch.cuda.synchronize()
     finally:
-        sq.set_option(sq.SQ_OPT_PDL, old[0])
-        sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, old[1])
-    yr = X.copy()
-    for _ in range(3):
-        for r in refs:
-            yr = oracle.gemm(yr, r["Wq"], r["scales"], r["zeros"]).astype(np.float16)
-    yr = yr.astype(np.float64)
-    assert _rel_frob(y, yr) <= 1e-2
+        sq.set_option(sq.SQ_OPT_PDL, old)
+    for i in range(1, len(ys)):
+        r = refs[(i - 1) % len(refs)]
+        xin = ys[i - 1].cpu().numpy()
+        y_ref = oracle.gemm(xin, r["Wq"], r["scales"], r["zeros"])
+        W_hat = oracle.dequant(r["Wq"], r["scales"], r["zeros"])
+        GemmCase(ys[i], y_ref, xin.astype(np.float64), W_hat, "f16").check(torch.float16)
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
@@ -269,36 +288,12 @@ def test_gemm_prefill_streamk(M, N, K, dtype):
     units are split between CTAs (stream-K) and finished by the fixup: ragged token
     tiles, whole tiles in the middle of a CTA's range, several CTAs per tile.  Bit-identical
     on every launch (fixed summation order)."""
-    y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M + N)
-    err = _rel_frob(y, y_ref)
-    assert err <= TOL_FROB and err <= TIGHT[dtype], err
+    _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M + N).check(dtype)
     x = torch.randn(M, K, device=DEV).to(dtype)
     q = sq.quantize_pack_groupwise(torch.randn(N, K, device=DEV).half() * 0.02)
     ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_PREFILL) for _ in range(3)]
     torch.cuda.synchronize()
     assert all(torch.equal(ys[0], yy) for yy in ys[1:])
-
-
-@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("M", [1, 3, 8, 9, 16])
-@pytest.mark.parametrize("N,K", [(512, 512), (264, 1152), (2048, 4096), (8192, 8192)])
-def test_gemm_decode_tcgen05_parity(M, N, K, dtype):
-    """The tcgen05 decode kernel (SQ_OPT_DECODE_KERNEL = SQ_DECK_TCGEN05): ragged row
-    blocks (N = 264), ragged 4-group stages (K = 1152 = 9 groups), stream-K fixups and a
-    wrapping stage ring (8192 x 8192), against the oracle; deterministic."""
-    sq.set_option(sq.SQ_OPT_DECODE_KERNEL, sq.SQ_DECK_TCGEN05)
-    try:
-        y, y_ref = _gemm_case(M, N, K, dtype, sq.SQ_PATH_DECODE, seed=M + 7, smooth=N <= 2048)
-        err = _rel_frob(y, y_ref)
-        assert err <= TOL_FROB and err <= TIGHT[dtype], err
-        if N == 8192:
-            x = torch.randn(M, K, device=DEV).to(dtype)
-            q = sq.quantize_pack_groupwise(torch.randn(N, K, device=DEV).half() * 0.02)
-            ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE) for _ in range(3)]
-            torch.cuda.synchronize()
-            assert all(torch.equal(ys[0], yy) for yy in ys[1:])
-    finally:
-        sq.set_option(sq.SQ_OPT_DECODE_KERNEL, sq.SQ_DECK_MMA_SYNC)
 
 
 @pytest.mark.parametrize("sched", ["streamk", "rowblock"])
@@ -320,7 +315,8 @@ def test_gemm_decode_schedules_shared_workspace(sched):
                 y_ref = oracle.gemm(X, ref["Wq"], ref["scales"], ref["zeros"], 128, "f16")
                 ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE) for _ in range(2)]
                 torch.cuda.synchronize()
-                assert _rel_frob(ys[0], y_ref) <= TIGHT[torch.float16], (N, K, M)
+                W_hat = oracle.dequant(ref["Wq"], ref["scales"], ref["zeros"])
+                GemmCase(ys[0], y_ref, X.astype(np.float64), W_hat, "f16").check(torch.float16)
                 assert torch.equal(ys[0], ys[1]), (N, K, M)
     finally:
         sq.set_option(sq.SQ_OPT_DECODE_SCHEDULE, sq.SQ_SCHED_AUTO)
@@ -342,7 +338,33 @@ def test_gemm_decode_streamk_fixup(M, dtype):
     y_ref = oracle.gemm(xn, ref["Wq"], ref["scales"], ref["zeros"], 128, xd)
     ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE) for _ in range(3)]
     torch.cuda.synchronize()
+    W_hat = oracle.dequant(ref["Wq"], ref["scales"], ref["zeros"])
     for y in ys:
-        assert _rel_frob(y, y_ref) <= TIGHT[dtype]
+        GemmCase(y, y_ref, x.float().cpu().double().numpy(), W_hat, xd).check(dtype)
     # deterministic: identical bits on every launch
     assert all(torch.equal(ys[0], y) for y in ys[1:])
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("path,M", [(sq.SQ_PATH_DECODE, 1), (sq.SQ_PATH_DECODE, 16), (sq.SQ_PATH_PREFILL, 40),
+                                    (sq.SQ_PATH_PREFILL, 300)])
+def test_gemm_edge_groups(path, M, dtype):
+    """The quantizer's edge-group suite (constant, one-sided, tie, subnormal, ±65504 and
+    −0.0 groups) as GEMM weights, through both paths.  Decode applies Δ
+    to the fp32 sum, so every output obeys the element-wise bound.  Prefill feeds
+    Ŵ = RN((q − Z)·Δ) to the tensor cores in the activation dtype: for fp16 a group whose
+    |(q − Z)·Δ| exceeds 65504 saturates to ±65504 (include/libsq.h), so those rows are
+    checked to be finite and the others against the bound."""
+    E = synth.edge_groups(128, seed=5)
+    R = E.shape[0]
+    N = (R + 63) // 64 * 64
+    W = np.concatenate([E, synth.weights(N - R, 128, seed=6)]).astype(np.float16)
+    W = np.concatenate([W, W[:, ::-1], synth.weights(N, 128, seed=7)], axis=1)   # K = 384
+    c = _gemm_case(M, N, 384, dtype, path, seed=3, smooth=False, W=W, x_scale=1e-3)
+    y = c.y.float().cpu().double().numpy()
+    assert np.isfinite(y).all()
+    ok_rows = np.ones(N, bool)
+    if path == sq.SQ_PATH_PREFILL and dtype == torch.float16:
+        ok_rows = np.abs(c.W_hat).max(axis=1) <= 65504.0
+    ratio = elementwise_ratio(y[:, ok_rows], c.y_ref[:, ok_rows], c.x64, c.W_hat[ok_rows], c.xd)
+    assert ratio <= 1.0, ratio

@@ -482,3 +482,46 @@ def test_n3_fold_rows_exact_rational_and_mlp_equivalence():
     assert np.linalg.norm(exact - ref) <= 1e-12 * np.linalg.norm(ref)
     stored = (x @ got.astype(np.float64).T) @ oracle.fold(Wdn, s).T
     assert np.linalg.norm(stored - ref) <= 2e-3 * np.linalg.norm(ref)
+
+
+def _bf16_bits_to_fraction(b: int):
+    v = float(np.array([int(b) << 16], dtype=np.uint32).view(np.float32)[0])
+    return v, (Fraction(v) if np.isfinite(v) else None)
+
+
+def test_rn_bf16_bits_against_exact():
+    """oracle.rn_bf16_bits decides every bf16 bit-exact test (S17 fold, bf16 X/s, bf16
+    fold_rows).  Pinned here against an exact-rational RN-even to bf16 (third
+    implementation, tests/exact_rational.py) on random fp64 values over the whole bf16
+    exponent range, exact midpoints (ties to even), subnormal values and ties,
+    the overflow threshold, signed zeros and non-finite inputs."""
+    r = np.random.default_rng(2024)
+    xs = list(r.standard_normal(600) * 2.0 ** r.integers(-140, 128, 600))
+    # exact midpoints between consecutive bf16 values (normal and subnormal binades),
+    # and values one fp64 ulp either side of them
+    for _ in range(300):
+        e = int(r.integers(-133, 127))
+        m = int(r.integers(0, 256))
+        q = 2.0 ** (max(e, -126) - 7) if e >= -126 else 2.0 ** -133
+        base = (m + (128 if e >= -126 else 0)) * q
+        mid = base + q / 2
+        for v in (mid, np.nextafter(mid, 0.0), np.nextafter(mid, np.inf)):
+            xs.append(float(v) * (1 if r.integers(0, 2) else -1))
+    big = float((2 - 2.0 ** -7) * 2.0 ** 127)
+    thr = float((2 - 2.0 ** -8) * 2.0 ** 127)            # midpoint BF16_MAX .. 2^128
+    xs += [big, -big, thr, -thr, float(np.nextafter(thr, 0.0)), 2.0 ** -133, 2.0 ** -134,
+           float(np.nextafter(2.0 ** -134, 1.0)), 3 * 2.0 ** -134, 1e-45, 1.0, -1.0]
+    got = oracle.rn_bf16_bits(np.array(xs, dtype=np.float64))
+    for x, b in zip(xs, got):
+        want = ex.rn_bf16(Fraction(x))
+        v, fv = _bf16_bits_to_fraction(b)
+        if want is None:
+            assert np.isinf(v) and np.signbit(v) == (x < 0), x
+        else:
+            assert fv == want, (x, hex(int(b)))
+            if want == 0:
+                assert np.signbit(v) == np.signbit(x), x   # sign of zero kept
+    # special values
+    sp = oracle.rn_bf16_bits(np.array([0.0, -0.0, np.inf, -np.inf, np.nan]))
+    assert [int(v) for v in sp[:4]] == [0x0000, 0x8000, 0x7F80, 0xFF80]
+    assert (int(sp[4]) & 0x7F80) == 0x7F80 and (int(sp[4]) & 0x007F) != 0

@@ -10,6 +10,16 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2312_03788_b200 import sq  # noqa: E402
 
+def _peaks():
+    try:
+        d = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+        return d["hbm_gbs"], d["bf16_tflops"]
+    except Exception:
+        return 6433.0, 1618.0
+
+
+PEAK_HBM, PEAK_TC = _peaks()
 SHAPES = {"o": (8192, 8192), "gate": (8192, 22016), "gate_up": (8192, 44032), "down": (22016, 8192)}
 
 
@@ -19,10 +29,13 @@ def bind(path):
     L = ctypes.CDLL(path)
     vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
     L.sq_w4a16_gemm_path.argtypes = [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]
+    if hasattr(L, "sq_w4a16_gemm_ex"):
+        L.sq_w4a16_gemm_ex.argtypes = [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, ctypes.c_uint, vp]
     L.sq_w4a16_gemm_workspace_bytes.argtypes = [i64, i64, i64, i32]
     L.sq_w4a16_gemm_workspace_bytes.restype = sz
     L.sq_set_option.argtypes = [i32, i32]
-    L.sq_set_option(2, 1)  # weights static
+    if not hasattr(L, "sq_w4a16_gemm_ex"):
+        L.sq_set_option(2, 1)  # version-1 libraries: process-wide "weights static"
     for kv in filter(None, opts.split(",")):
         k, v = kv.split("=")
         assert L.sq_set_option(int(k), int(v)) == 0
@@ -65,9 +78,12 @@ def main():
                 ws = torch.zeros(nb + 256, dtype=torch.uint8, device=dev)
 
                 def call(q, L=L, ws=ws, nb=nb):
-                    st = L.sq_w4a16_gemm_path(x.data_ptr(), 0, q.Wq.data_ptr(), q.scales.data_ptr(),
-                                              q.zeros.data_ptr(), y.data_ptr(), M, N, K, 128, ws.data_ptr(),
-                                              nb + 256, path, torch.cuda.current_stream().cuda_stream)
+                    args = (x.data_ptr(), 0, q.Wq.data_ptr(), q.scales.data_ptr(), q.zeros.data_ptr(), y.data_ptr(),
+                            M, N, K, 128, ws.data_ptr(), nb + 256, path)
+                    if hasattr(L, "sq_w4a16_gemm_ex"):  # weights resident and final: SQ_GEMM_WEIGHTS_STATIC
+                        st = L.sq_w4a16_gemm_ex(*args, 1, torch.cuda.current_stream().cuda_stream)
+                    else:
+                        st = L.sq_w4a16_gemm_path(*args, torch.cuda.current_stream().cuda_stream)
                     assert st == 0, st
                 for q in qs:
                     call(q)
@@ -90,13 +106,13 @@ def main():
                     times[lname].append(e0.elapsed_time(e1) * 1e3 / launches)
             B = wb + 2 * M * K + 2 * M * N
             if path == 2 and M >= 128:
-                B = 2 * M * N * K * 6532.2 / 1657.7  # report the fraction of the dense fp16 peak
+                B = 2 * M * N * K * PEAK_HBM / PEAK_TC  # report the fraction of the dense fp16 peak
             row = {"shape": name, "M": M}
             for ln, ts in times.items():
                 ts = sorted(ts)[1:-1]
                 us = sum(ts) / len(ts)
                 row[ln] = round(us, 2)
-                row[ln + "_frac"] = round(B / (us * 1e-6) / 1e9 / 6532.2, 3)
+                row[ln + "_frac"] = round(B / (us * 1e-6) / 1e9 / PEAK_HBM, 3)
             print(json.dumps(row), flush=True)
             del graphs
         del qs, q0

@@ -47,9 +47,8 @@ def main():
     W = (torch.randn(N, K, device=dev) * 0.02).half()
     q0 = sq.quantize_pack_groupwise(W)
     del W
-    qs = [q0] + [sq.QuantizedLinear(q0.Wq.clone(), q0.scales.clone(), q0.zeros.clone(), N, K)
+    qs = [q0] + [sq.QuantizedLinear(q0.Wq.clone(), q0.scales.clone(), q0.zeros.clone(), N, K, static=True)
                  for _ in range(copies - 1)]
-    sq.set_option(sq.SQ_OPT_WEIGHTS_STATIC, 1)
     rows = []
     best = {}
     for M in (int(v) for v in a.ms.split(",")):

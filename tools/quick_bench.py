@@ -28,7 +28,7 @@ def make_weights(K, N, copies, dev):
     del W
     out = [q]
     for _ in range(copies - 1):
-        out.append(sq.QuantizedLinear(q.Wq.clone(), q.scales.clone(), q.zeros.clone(), q.N, q.K))
+        out.append(sq.QuantizedLinear(q.Wq.clone(), q.scales.clone(), q.zeros.clone(), q.N, q.K, static=True))
     return out
 
 
