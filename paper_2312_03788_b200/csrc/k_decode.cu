@@ -31,11 +31,14 @@
 #include <algorithm>
 #include <mutex>
 
+#include "decode_common.cuh"
 #include "sq_internal.cuh"
 
 namespace sq {
 
 namespace {
+
+using namespace dec;
 
 constexpr int kGroup = 128;
 constexpr int GPS = 4;             // groups per stage (unit)
@@ -146,6 +149,16 @@ __device__ __forceinline__ void tma_3d_hint(uint32_t dst, const CUtensorMap* m, 
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy) : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n"
@@ -203,137 +216,6 @@ __device__ __forceinline__ void mma_16816_zc(float (&d)[4], uint32_t a0, uint32_
   }
 }
 
-__device__ __forceinline__ uint32_t hsub2_u(uint32_t a, uint32_t b, bool bf16) {
-  if (bf16) {
-    __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a),
-                               *reinterpret_cast<__nv_bfloat162*>(&b));
-    return *reinterpret_cast<uint32_t*>(&r);
-  }
-  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
-}
-__device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
-  __half2 r = __hfma2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b),
-                      *reinterpret_cast<__half2*>(&c));
-  return *reinterpret_cast<uint32_t*>(&r);
-}
-
-// One 32-bit word of codes (k offsets 0..7 of one row) -> the exact (q - Z) pairs
-// (e0,e4), (e1,e5), (e2,e6), (e3,e7) in fp16 / bf16.
-template <bool kBF16>
-__device__ __forceinline__ void dequant_word(uint32_t w, uint32_t zsub, uint32_t zfma, uint32_t (&h)[4]) {
-  if (!kBF16) {
-    const uint32_t t = w >> 8;
-    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x64006400u), zsub, false);  // 1024+q - (1024+Z)
-    h[2] = hsub2_u(lop3_and_or(t, 0x000F000Fu, 0x64006400u), zsub, false);
-    h[1] = hfma2_u(lop3_and_or(w, 0x00F000F0u, 0x64006400u), 0x2C002C00u, zfma);  // (1024+16q)/16-(64+Z)
-    h[3] = hfma2_u(lop3_and_or(t, 0x00F000F0u, 0x64006400u), 0x2C002C00u, zfma);
-  } else {
-    h[0] = hsub2_u(lop3_and_or(w, 0x000F000Fu, 0x43004300u), zsub, true);  // 128+q - (128+Z)
-    h[1] = hsub2_u(lop3_and_or(w >> 4, 0x000F000Fu, 0x43004300u), zsub, true);
-    h[2] = hsub2_u(lop3_and_or(w >> 8, 0x000F000Fu, 0x43004300u), zsub, true);
-    h[3] = hsub2_u(lop3_and_or(w >> 12, 0x000F000Fu, 0x43004300u), zsub, true);
-  }
-}
-
-// zero-point constants from the fp16 bits of Z (an integer 0..15)
-template <bool kBF16>
-__device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint32_t& zfma) {
-  const uint32_t z = (uint32_t)__half2int_rn(__ushort_as_half(zbits));
-  if (!kBF16) {
-    zsub = z * 0x00010001u + 0x64006400u;         // fp16x2(1024 + Z): ulp of 1024 is 1
-    zfma = z * 0x00100010u + 0xD400D400u;         // fp16x2(-(64 + Z)): ulp of 64 is 1/16
-  } else {
-    zsub = z * 0x00010001u + 0x43004300u;         // bf16x2(128 + Z): ulp of 128 is 1
-    zfma = 0;
-  }
-}
-
-// Work split.  Units are numbered u = rb * upb + pos (row block rb, stage pos).
-//  stream-K (dp = 0): CTA c owns the contiguous range [start(c), start(c + 1)).
-//  row-block (dp = 1): CTA c owns row blocks c, c + P, c + 2P, ... (each a full range).
-struct Work {
-  int units, upb, cta_q, cta_r, rbs, dp;
-  __device__ __forceinline__ int start(int c) const { return c * cta_q + min(c, cta_r); }
-  __device__ __forceinline__ int cta_of(int u) const {
-    const int big = (cta_q + 1) * cta_r;
-    return u < big ? u / (cta_q + 1) : cta_r + (u - big) / cta_q;
-  }
-};
-
-// Walks the units of one CTA in processing order (identical in all three warp roles) as
-// segments: contiguous unit ranges inside one row block.  Stream-K processes a CTA's
-// partial row blocks (the head and tail of its range) FIRST and its whole row blocks
-// after them, so the fixups of cut row blocks overlap the rest of the stream and the
-// kernel ends on plain Y stores instead of fixup round trips.
-struct Sched {
-  int c, P, ri, nr, u, ue;
-  int u0, u1, hp, tp, nparts, f_lo;
-  bool full;  // the segment is a whole row block (direct Y store)
-  int e;      // partial-slot index: 0 = head of the CTA's range, 1 = tail
-  __device__ __forceinline__ Sched(const Work& wk, int c_, int P_) : c(c_), P(P_), ri(0) {
-    if (wk.dp) {
-      nr = (wk.rbs - c + P - 1) / P;
-    } else {
-      u0 = wk.start(c);
-      u1 = wk.start(c + 1);
-      const int rb_a = u0 / wk.upb, rb_b = (u1 - 1) / wk.upb;
-      if (rb_a == rb_b) {
-        hp = 1;
-        tp = 0;
-        nparts = 1;
-        nr = 1;
-      } else {
-        hp = u0 % wk.upb != 0;
-        tp = u1 % wk.upb != 0;
-        nparts = hp + tp;
-        f_lo = hp ? rb_a + 1 : rb_a;
-        const int f_hi = tp ? rb_b - 1 : rb_b;
-        nr = nparts + max(0, f_hi - f_lo + 1);
-      }
-    }
-    load(wk);
-  }
-  __device__ __forceinline__ void load(const Work& wk) {
-    if (ri >= nr) return;
-    if (wk.dp) {
-      u = (c + ri * P) * wk.upb;
-      ue = u + wk.upb;
-      full = true;
-      e = 0;
-    } else if (nr == 1 && nparts == 1 && hp && (u1 - 1) / wk.upb == u0 / wk.upb) {
-      u = u0;  // the whole range lies in one row block
-      ue = u1;
-      full = (u0 % wk.upb == 0) && (u1 - u0 == wk.upb);
-      e = 0;
-    } else if (ri < nparts) {
-      if (hp && ri == 0) {
-        u = u0;
-        ue = (u0 / wk.upb + 1) * wk.upb;
-        e = 0;
-      } else {
-        u = ((u1 - 1) / wk.upb) * wk.upb;
-        ue = u1;
-        e = 1;
-      }
-      full = false;
-    } else {
-      u = (f_lo + ri - nparts) * wk.upb;
-      ue = u + wk.upb;
-      full = true;
-      e = 0;
-    }
-  }
-  __device__ __forceinline__ bool valid() const { return ri < nr; }
-  __device__ __forceinline__ bool range_last() const { return u + 1 == ue; }
-  __device__ __forceinline__ void next(const Work& wk) {
-    if (++u == ue) {
-      ++ri;
-      load(wk);
-    }
-  }
-};
-
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 // Row-parallel all-reduce fused into the epilogue (sq_w4a16_gemm_allreduce; the buffer
@@ -372,7 +254,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(bar_full + 8 * i, 1);
       mbar_init(bar_empty + 8 * i, C::CW);
-      mbar_init(red_full + 8 * i, C::CW);
+      mbar_init(red_full + 8 * i, C::CW * 32);  // every consumer lane arrives after its parked writes
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -407,6 +289,16 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
           mbar_expect_tx(fb, C::TX);
           load_weights(sbase + pre * C::STAGE, fb, sc.u);
         }
+#ifdef SQ_DEC_L2PF
+        // the units after the ring: HBM -> L2 while this kernel waits for its predecessor
+        // (and while the predecessor's tail runs), so the startup bubble streams weights
+        for (int k = 0; k < SQ_DEC_L2PF && sc.valid(); ++k, sc.next(wk)) {
+          const int rb = sc.u / wk.upb, g0 = (sc.u % wk.upb) * GPS;
+          tma_prefetch_l2_3d(&tm_w, 0, rb * BN, g0);
+          tma_prefetch_l2_2d(&tm_s, rb * BN, g0);
+          tma_prefetch_l2_2d(&tm_z, rb * BN, g0);
+        }
+#endif
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
       int s = 0;
@@ -719,10 +611,10 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
           for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.0f;
         }
       // the stage is refilled by TMA (async proxy) after the epilogue releases it: order
-      // these generic-proxy writes before that
+      // these generic-proxy writes before that.  Every lane arrives (release) after its own
+      // writes, so the epilogue's acquire covers all of them directly.
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(red_full + 8 * s);
+      mbar_arrive(red_full + 8 * s);
     }
     if (++s == C::NS) { s = 0; ph ^= 1; }
   }
@@ -782,7 +674,7 @@ int ctas_per_sm() {
 template <int MT, bool kBF16, int BN, int XR, int CT>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, bool weights_static,
-                     cudaStream_t st, const char** why) {
+                     int grid_per_sm, cudaStream_t st, const char** why) {
   using C = Cfg<MT, BN, XR, CT>;
   const int G = K / kGroup;
   CUtensorMap tw, tx, ts, tz;
@@ -819,7 +711,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   wk.upb = (G + GPS - 1) / GPS;
   wk.units = wk.rbs * wk.upb;
   wk.dp = dp ? 1 : 0;
-  int slots = num_sms() * ctas_per_sm<MT, kBF16, BN, XR, CT>();
+  int slots = num_sms() * std::min(grid_per_sm, ctas_per_sm<MT, kBF16, BN, XR, CT>());
   if (option(SQ_OPT_DECODE_GRID_LIMIT) > 0) slots = std::min(slots, option(SQ_OPT_DECODE_GRID_LIMIT));
   const int P = dp ? std::min(wk.rbs, slots) : std::min(wk.units, slots);
   wk.cta_q = wk.units / P;
@@ -872,9 +764,9 @@ bool auto_rowblock(int N, int K, int slots, int* bn_out) {
 template <int MT, bool kBF16, int XR, int CT>
 cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, const ArParams& ar, bool weights_static,
-                     cudaStream_t st, const char** why) {
+                     cudaStream_t st, const char** why, int grid_per_sm = CT) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
-  const int slots = num_sms() * CT;
+  const int slots = num_sms() * grid_per_sm;
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
   // blocks (no stream-K fixups) when one wave of them fits the resident CTA slots, a CTA's
   // row block exceeds the stream-K share by at most what the fixups cost (~2.5 µs at a CTA's
@@ -903,11 +795,19 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     dp = false;
     bn = 64;
   }
-  if (bn == 32) return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, st, why);
-  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, st, why);
+  if (bn == 32)
+    return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, grid_per_sm,
+                                           st, why);
+  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, grid_per_sm, st,
+                                         why);
 }
 
 }  // namespace
+
+bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  return encode(map, dt, rank, base, dims, strides_bytes, box, sw);
+}
 
 size_t decode_partials_bytes() {
   return (size_t)num_sms() * kMaxCtasPerSm * 2 * 16 * kMaxBN * sizeof(float);
@@ -923,6 +823,14 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
                           cudaStream_t st, const char** why, const ArParams* ar_in) {
   const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
+#ifdef SQ_DEC_M1_SLOT3
+  // experiment: M = 1 with the 74-KB three-CTA configuration but only two CTAs per SM, so
+  // the next kernel's first CTAs can become resident (and stream their weights) in the
+  // third slot while this kernel's tail runs
+  if (M == 1 && ar.world == 0)
+    return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why, 2)
+                : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why, 2);
+#endif
   if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
     // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
     // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);

@@ -191,61 +191,48 @@ def test_fused_allreduce_34b_tp_shards(P, layer, dtype, grid_limit):
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 def test_fused_allreduce_back_to_back_pdl(dtype):
-    """Several fused calls on one stream per rank with NO host synchronization in between,
-    programmatic dependent launch on, device-managed epochs (epoch 0), interleaved with
-    plain GEMMs on the same streams (the epoch must be read only after the
-    previous call's grid completed).  Every call's result is checked afterwards."""
-    from paper_2312_03788_b200 import synth, tp
+    """Back-to-back fused calls on one stream with NO host synchronization, programmatic
+    dependent launch on, device-managed epochs (epoch 0), interleaved with plain GEMMs
+    (a call must read the epoch only after the previous call's grid completed,
+    or two calls share an epoch).  One rank, so no cross-rank scheduling is involved (two
+    simulated ranks on one GPU can starve each other's streams, which separate GPUs
+    cannot): the buffer's epoch must advance by exactly one per call, no error may be
+    raised, and every result must equal the same call made in isolation (deterministic)."""
+    from paper_2312_03788_b200 import synth
 
-    world, M, N, K = 2, 4, 1024, 2048
-    W = torch.from_numpy(synth.weights(N, K, seed=5)).to(DEV)
-    ranges = tp.channel_split(K, world)
-    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()).mark_static() for a, b in ranges]
-    q_plain = sq.quantize_pack_groupwise(W[:, :1024].contiguous()).mark_static()
+    M, N, K = 4, 1024, 2048
+    q = sq.quantize_pack_groupwise(torch.from_numpy(synth.weights(N, K, seed=5)).to(DEV)).mark_static()
+    qp = sq.quantize_pack_groupwise(torch.from_numpy(synth.weights(N, 1024, seed=6)).to(DEV)).mark_static()
     n_max = M * N
-    nb = sq.allreduce_buffer_bytes(n_max, world)
-    bufs = [torch.zeros(nb, dtype=torch.uint8, device=DEV) for _ in range(world)]
-    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
-    errs = [torch.zeros(1, dtype=torch.int32, device=DEV) for _ in range(world)]
-    wss = [torch.zeros(sq.w4a16_gemm_workspace_bytes(M, N, K), dtype=torch.uint8, device=DEV) for _ in range(world)]
-    streams = [torch.cuda.Stream() for _ in range(world)]
+    buf = torch.zeros(sq.allreduce_buffer_bytes(n_max, 1), dtype=torch.uint8, device=DEV)
+    peers = torch.tensor([buf.data_ptr()], dtype=torch.int64, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(sq.w4a16_gemm_workspace_bytes(M, N, K), dtype=torch.uint8, device=DEV)
     g = torch.Generator(device=DEV).manual_seed(11)
-    calls = 8
-    Xs = [(torch.randn(M, K, generator=g, device=DEV)).to(dtype) for _ in range(calls)]
-    outs = [[torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)] for _ in range(calls)]
-    plain = [[None] * world for _ in range(calls)]
+    calls = 12
+    Xs = [torch.randn(M, K, generator=g, device=DEV).to(dtype) for _ in range(calls)]
+    outs = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(calls)]
+    plain = [None] * calls
     old = sq.get_option(sq.SQ_OPT_PDL)
     sq.set_option(sq.SQ_OPT_PDL, 1)
     try:
         torch.cuda.synchronize()
-        for r in range(world):
-            with torch.cuda.stream(streams[r]):
-                for c in range(calls):
-                    a, b = ranges[r]
-                    sq.w4a16_gemm_allreduce(Xs[c][:, a:b].contiguous(), qs[r], peers, r, world, n_max, errs[r],
-                                            out=outs[c][r], workspace=wss[r], stream=streams[r])
-                    if c % 3 == 1:  # a plain decode GEMM between two fused calls
-                        plain[c][r] = sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), q_plain, workspace=wss[r],
-                                                    stream=streams[r])
+        for c in range(calls):
+            sq.w4a16_gemm_allreduce(Xs[c], q, peers, 0, 1, n_max, err, out=outs[c], workspace=ws)
+            if c % 3 == 1:  # a plain decode GEMM between two fused calls, same workspace
+                plain[c] = sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), qp, workspace=ws)
         torch.cuda.synchronize()
     finally:
         sq.set_option(sq.SQ_OPT_PDL, old)
-    assert all(int(e.item()) == 0 for e in errs)
+    assert int(err.item()) == 0
+    assert int(buf[:4].view(torch.int32).item()) == calls   # one epoch per call
     for c in range(calls):
-        # the same call again, isolated (synchronized before and after): deterministic
-        ref = [torch.empty(M, N, dtype=dtype, device=DEV) for _ in range(world)]
-        for r in range(world):
-            with torch.cuda.stream(streams[r]):
-                a, b = ranges[r]
-                sq.w4a16_gemm_allreduce(Xs[c][:, a:b].contiguous(), qs[r], peers, r, world, n_max, errs[r],
-                                        out=ref[r], workspace=wss[r], stream=streams[r])
+        ref = sq.w4a16_gemm_allreduce(Xs[c], q, peers, 0, 1, n_max, err, workspace=ws)
         torch.cuda.synchronize()
-        for r in range(world):
-            assert torch.equal(outs[c][r].view(torch.int16), outs[c][0].view(torch.int16)), (c, r)
-            assert torch.equal(outs[c][r].view(torch.int16), ref[r].view(torch.int16)), (c, r)
-            if plain[c][r] is not None:
-                assert torch.equal(plain[c][r], sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), q_plain)), (c, r)
-    assert all(int(e.item()) == 0 for e in errs)
+        assert torch.equal(outs[c].view(torch.int16), ref.view(torch.int16)), c
+        if plain[c] is not None:
+            assert torch.equal(plain[c], sq.w4a16_gemm(Xs[c][:, :1024].contiguous(), qp)), c
+    assert int(err.item()) == 0
 
 
 def _free_port():

@@ -87,3 +87,59 @@ def test_tp_world2_one_gpu():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def _nccl_worker(port, q):
+    """One rank, NCCL process group (init_process_group("nccl", device_id=...)) as bench.py
+    does for N > 1: the row-parallel layers of a 1-rank stack reduced through the NCCL
+    fallback (fp16 in place, bf16 through an fp32 copy) and through the peer-memory path
+    (attach_peer_allreduce: IPC setup, validation, fused GEMM + all-reduce kernel) must
+    equal the plain GEMM of the same shard -- a 1-rank sum is the partial itself."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+        from paper_2312_03788_b200 import sq, stack, tp
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+        model = tp.ModelShape("tiny-34b-like", hidden=1024, mlp=2816, layers=2, q_heads=8, kv_heads=2,
+                              head_dim=128)
+        st = stack.build_stack(model, 2, 0, 1, dev, group=pg)
+        ok = []
+        for dt in (torch.float16, torch.bfloat16):
+            st.dtype = dt
+            for M in (1, 16, 40):
+                b = stack.make_buffers(st, M, dev)
+                stack.run_pass(st, b)               # NCCL all_reduce after row-parallel layers
+                torch.cuda.synchronize()
+                for lin in st.layers[-1]:
+                    want = sq.w4a16_gemm(b.x[lin.shard.name], lin.q)
+                    ok.append(bool(torch.equal(b.y[lin.shard.name], want)))
+        impl = stack.attach_peer_allreduce(st, 16 * model.hidden, dev)
+        ok.append(impl.startswith("peer"))
+        st.dtype = torch.float16
+        for M in (1, 16):
+            b = stack.make_buffers(st, M, dev)
+            stack.run_pass(st, b)                   # fused GEMM + peer all-reduce (1 rank)
+            torch.cuda.synchronize()
+            for lin in st.layers[-1]:
+                want = sq.w4a16_gemm(b.x[lin.shard.name], lin.q).float()
+                got = b.y[lin.shard.name].float()
+                ok.append(bool(((got - want).abs() <= 2e-3 * want.abs() + 1e-3).all()))
+        ok.append(not st.peer_ar.failed())
+        q.put(all(ok) or f"failed: {ok} ({impl})")
+    except Exception as e:
+        q.put(repr(e))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_nccl_process_group_one_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=600)
+    p.join(timeout=60)
+    assert res is True, res

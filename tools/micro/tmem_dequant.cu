@@ -95,6 +95,12 @@ __global__ void kern(int iters, int tmem_cols, float* out, long long* clk) {
     const float d = __half2float(__ushort_as_half(lds16(sbase + 4 * 8192 + st * 512 + row * 2)));
     const uint32_t zs = zq * 0x00010001u + 0x64006400u, zf = zq * 0x00100010u + 0xD400D400u;
     uint32_t a[64];
+    uint32_t v[NT > 0 ? NT : 1];
+    if (NT > 0) {  // readback of an older group's accumulator, issued before this group's math
+#pragma unroll
+      for (int h = 0; h < NT / 8; ++h)
+        tld8(tmem + lane_addr + (uint32_t)(h * 8), *reinterpret_cast<uint32_t(*)[8]>(&v[h * 8]));
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const uint32_t t = w[k] >> 8;
@@ -108,14 +114,9 @@ __global__ void kern(int iters, int tmem_cols, float* out, long long* clk) {
     tst32(abase + 32, a + 32);
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     if (NT > 0) {
-      uint32_t v[8];
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-      for (int h = 0; h < NT / 8; ++h) {
-        tld8(tmem + lane_addr + (uint32_t)(h * 8), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-        for (int t = 0; t < 8; ++t) acc[h * 8 + t] = fmaf(__uint_as_float(v[t]), d, acc[h * 8 + t]);
-      }
+      for (int t = 0; t < NT; ++t) acc[t] = fmaf(__uint_as_float(v[t]), d, acc[t]);
     }
   }
   float s = 0.f;
@@ -165,7 +166,7 @@ int main() {
   long long* clk;
   cudaMalloc(&out, 16);
   cudaMalloc(&clk, 4096 * sizeof(long long));
-  for (int w : {4, 8, 12, 16}) {
+  for (int w : {4, 8, 12}) {
     run<0>(sms, w, 1, out, clk);
     run<8>(sms, w, 1, out, clk);
     run<16>(sms, w, 1, out, clk);

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--K", type=int, default=8192)
     ap.add_argument("--N", type=int, default=22016)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--path", type=int, default=None, help="explicit SQ_PATH_* (3 = tcgen05 decode)")
     a = ap.parse_args()
     dev = "cuda"
     W = (torch.randn(a.N, a.K, device=dev) * 0.02).half()
@@ -35,6 +36,8 @@ def main():
         x = torch.randn(M, a.K, device=dev).half()
         y = torch.empty(M, a.N, device=dev, dtype=torch.half)
         path = sq.SQ_PATH_DECODE if a.kind == "decode" else sq.SQ_PATH_PREFILL
+        if a.path is not None:
+            path = a.path
         nb = sq.w4a16_gemm_workspace_bytes(M, a.N, a.K)
         ws = torch.zeros(max(nb, 16), dtype=torch.uint8, device=dev)
         for _ in range(a.reps):
