@@ -53,9 +53,11 @@ constexpr int kMinBN = 32;
 constexpr uint32_t kIdleWaitNs = 100000;
 
 // MT: 8-token MMA n-tiles; XR: token rows of the activation box actually staged (M = 1 stages
-// one row, the MMA sees zeros for the other seven); CT: resident CTAs per SM (smem budget)
-template <int MT, int BN, int XR, int CT>
+// one row, the MMA sees zeros for the other seven); CT: resident CTAs per SM (smem budget);
+// GS: quantization group size (128, or 64 / 32: "different group sizes")
+template <int MT, int BN, int XR, int CT, int GS = 128>
 struct Cfg {
+  static constexpr int SUB = kGroup / GS;                 // groups per 128-k slot
   static constexpr int MPAD = 8 * MT;
   static constexpr int CW = kConsumerWarps;
   static constexpr int THREADS = (CW + 2) * 32;
@@ -64,7 +66,7 @@ struct Cfg {
   static constexpr int RT = BN / 16;                      // 16-row tiles per consumer warp
   static constexpr int CODES = GPS * BN * (kGroup / 2);  // 16 KB at BN = 64
   static constexpr int XB = GPS * XR * kGroup * 2;        // 1 / 8 / 16 KB
-  static constexpr int SZ = GPS * BN * 2;
+  static constexpr int SZ = GPS * SUB * BN * 2;           // Δ (or Z) rows of the stage: [slot][sub][row]
   // stage bases stay 1024-B aligned (SWIZZLE_128B destination of the X box)
   static constexpr int TX = CODES + XB + 2 * SZ;  // bytes the TMA delivers per stage
   static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
@@ -216,6 +218,37 @@ __device__ __forceinline__ void mma_16816_zc(float (&d)[4], uint32_t a0, uint32_
   }
 }
 
+// h[i] (exact (q - Z) pairs) <- RN((q - Z) Δ) in the activation format, Δ = fp16 bits.
+// fp16: one HMUL2 per pair; a Δ above 65504 / 15 could overflow, so such a (row, group) --
+// impossible for real weights -- takes the fp32 product clamped to ±65504.
+template <bool kBF16>
+__device__ __forceinline__ void scale_pairs(uint32_t (&h)[4], uint16_t dbits) {
+  const float df = __half2float(__ushort_as_half(dbits));
+  if (kBF16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[i]));
+      const __nv_bfloat162 b = __floats2bfloat162_rn(f.x * df, f.y * df);  // exact product, one RN
+      h[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+  } else if (df > 4366.0f) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[i]));
+      const __half2 r = __floats2half2_rn(fminf(fmaxf(f.x * df, -65504.0f), 65504.0f),
+                                          fminf(fmaxf(f.y * df, -65504.0f), 65504.0f));
+      h[i] = *reinterpret_cast<const uint32_t*>(&r);
+    }
+  } else {
+    const __half2 d2 = __half2half2(__ushort_as_half(dbits));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&h[i]), d2);
+      h[i] = *reinterpret_cast<const uint32_t*>(&r);
+    }
+  }
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 // Row-parallel all-reduce fused into the epilogue (sq_w4a16_gemm_allreduce; the buffer
@@ -233,13 +266,13 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-template <int MT, bool kBF16, int BN, int XR, int CT, bool kAR>
-__global__ void __launch_bounds__(Cfg<MT, BN, XR, CT>::THREADS, CT)
+template <int MT, bool kBF16, int BN, int XR, int CT, bool kAR, int GS>
+__global__ void __launch_bounds__(Cfg<MT, BN, XR, CT, GS>::THREADS, CT)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
               int M, int N, Work wk, int early_weights, const ArParams ar) {
-  using C = Cfg<MT, BN, XR, CT>;
+  using C = Cfg<MT, BN, XR, CT, GS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -275,8 +308,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       auto load_weights = [&](uint32_t st, uint32_t fb, int u) {
         const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
         tma_3d_hint(st, &tm_w, fb, 0, rb * BN, g0, wpol);
-        tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0);
-        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0);
+        tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0 * C::SUB);
+        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0 * C::SUB);
       };
       // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
       // declared them static (SQ_GEMM_WEIGHTS_STATIC): stream the first stages before
@@ -549,6 +582,37 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     const uint32_t cbase = st + grp * (BN * 64) + r * 64 + j * 16;
     const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
     const uint32_t sbz = sbs + C::SZ;
+    if constexpr (GS < kGroup) {
+      // groups of 64 / 32 k: one MMA's 16 k span the four lanes' 32-k ranges, i.e. up to
+      // four groups, so Δ cannot be applied to the fp32 sum; the operand is the rounded
+      // Ŵ = RN((q - Z) Δ) instead (the value the prefill path feeds its MMA, P13) and the
+      // MMA accumulates Ŵ·X directly.  Lane j's k range lies in group (32 j) / GS.
+      const uint32_t sbg = st + C::CODES + C::XB + ((grp * C::SUB + (32 * j) / GS) * BN + r) * 2;
+#pragma unroll
+      for (int rt = 0; rt < C::RT; ++rt) {
+        const uint4 ca = lds128(cbase + rt * 16 * 64);
+        const uint4 cb = lds128(cbase + (rt * 16 + 8) * 64);
+        const uint16_t dA = lds16(sbg + rt * 32), dB = lds16(sbg + rt * 32 + 16);
+        uint32_t zsA, zfA, zsB, zfB;
+        zero_consts<kBF16>(lds16(sbg + C::SZ + rt * 32), zsA, zfA);
+        zero_consts<kBF16>(lds16(sbg + C::SZ + rt * 32 + 16), zsB, zfB);
+        const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
+        const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint32_t hA[4], hB[4];
+          dequant_word<kBF16>(wa[w], zsA, zfA, hA);
+          dequant_word<kBF16>(wb[w], zsB, zfB, hB);
+          scale_pairs<kBF16>(hA, dA);
+          scale_pairs<kBF16>(hB, dB);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            mma_16816(acc[rt][mt], hA[0], hB[0], hA[1], hB[1], xb[mt][w][0], xb[mt][w][1], kBF16);
+            mma_16816(acc[rt][mt], hA[2], hB[2], hA[3], hB[3], xb[mt][w][2], xb[mt][w][3], kBF16);
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int rt = 0; rt < C::RT; ++rt) {
       const uint4 ca = lds128(cbase + rt * 16 * 64);
@@ -648,7 +712,7 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* base
 
 // Resident CTAs per SM of one kernel instance (occupancy query), cached per device: the
 // dynamic-smem attribute is per device context, so it is set on each device before use.
-template <int MT, bool kBF16, int BN, int XR, int CT>
+template <int MT, bool kBF16, int BN, int XR, int CT, int GS>
 int ctas_per_sm() {
   static int cached[64];
   static std::once_flag once[64];
@@ -658,25 +722,25 @@ int ctas_per_sm() {
   std::call_once(once[dev], [] {
     int d = 0, n = 0;
     cudaGetDevice(&d);
-    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
-    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<MT, BN, XR, CT>::SMEM_ALLOC);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT, false>,
-                                                      Cfg<MT, BN, XR, CT>::THREADS,
-                                                      Cfg<MT, BN, XR, CT>::SMEM_ALLOC) != cudaSuccess || n < 1)
+    using C = Cfg<MT, BN, XR, CT, GS>;
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, false, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM_ALLOC);
+    cudaFuncSetAttribute(decode_kernel<MT, kBF16, BN, XR, CT, true, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM_ALLOC);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<MT, kBF16, BN, XR, CT, false, GS>, C::THREADS,
+                                                      C::SMEM_ALLOC) != cudaSuccess || n < 1)
       n = 1;
     cached[d < 64 && d >= 0 ? d : 0] = std::min(n, CT);
   });
   return cached[dev];
 }
 
-template <int MT, bool kBF16, int BN, int XR, int CT>
+template <int MT, bool kBF16, int BN, int XR, int CT, int GS = 128>
 cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                      void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, bool weights_static,
                      int grid_per_sm, cudaStream_t st, const char** why) {
-  using C = Cfg<MT, BN, XR, CT>;
-  const int G = K / kGroup;
+  using C = Cfg<MT, BN, XR, CT, GS>;
+  const int G = K / kGroup;  // 128-k slots
   CUtensorMap tw, tx, ts, tz;
   {
     const uint64_t d[3] = {64, (uint64_t)N, (uint64_t)G};
@@ -697,9 +761,9 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     }
   }
   {
-    const uint64_t d[2] = {(uint64_t)N, (uint64_t)G};
+    const uint64_t d[2] = {(uint64_t)N, (uint64_t)G * C::SUB};  // [K / GS][N]
     const uint64_t s[1] = {(uint64_t)N * 2};
-    const uint32_t b[2] = {(uint32_t)BN, GPS};
+    const uint32_t b[2] = {(uint32_t)BN, (uint32_t)(GPS * C::SUB)};
     if (!encode(&ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, scales, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, zeros, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
       *why = "tensor map (scales/zeros)";
@@ -711,7 +775,7 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   wk.upb = (G + GPS - 1) / GPS;
   wk.units = wk.rbs * wk.upb;
   wk.dp = dp ? 1 : 0;
-  int slots = num_sms() * std::min(grid_per_sm, ctas_per_sm<MT, kBF16, BN, XR, CT>());
+  int slots = num_sms() * std::min(grid_per_sm, ctas_per_sm<MT, kBF16, BN, XR, CT, GS>());
   if (option(SQ_OPT_DECODE_GRID_LIMIT) > 0) slots = std::min(slots, option(SQ_OPT_DECODE_GRID_LIMIT));
   const int P = dp ? std::min(wk.rbs, slots) : std::min(wk.units, slots);
   wk.cta_q = wk.units / P;
@@ -732,10 +796,10 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && weights_static;
   if (ar.world > 0)
-    return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, true>, tw, tx, ts, tz, (uint16_t*)Y,
+    return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, true, GS>, tw, tx, ts, tz, (uint16_t*)Y,
                               counters, partials, M, N, wk, early, ar);
-  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, false>, tw, tx, ts, tz, (uint16_t*)Y, counters,
-                            partials, M, N, wk, early, ar);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, false, GS>, tw, tx, ts, tz, (uint16_t*)Y,
+                            counters, partials, M, N, wk, early, ar);
 }
 
 // Fraction of the resident CTA slots kept busy by whole row blocks of height bn.
@@ -818,11 +882,37 @@ size_t decode_workspace_bytes(int64_t N) {
   return ws_partials_bytes() + counter_region_bytes(RB);
 }
 
+template <int GS>
+cudaError_t launch_small_group(const void* X, bool bf16, const uint8_t* Wq, const uint16_t* scales,
+                               const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, const ArParams& ar,
+                               bool weights_static, cudaStream_t st, const char** why) {
+  // group sizes 64 / 32: one configuration per M class (stream-K, 64-row blocks, two CTAs per SM)
+  constexpr int C2 = kCtasPerSm;
+  if (M == 1)
+    return bf16 ? launch_t<1, true, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+                                                   st, why)
+                : launch_t<1, false, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static,
+                                                    C2, st, why);
+  if (M <= 8)
+    return bf16 ? launch_t<1, true, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+                                                   st, why)
+                : launch_t<1, false, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static,
+                                                    C2, st, why);
+  return bf16 ? launch_t<2, true, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+                                                  st, why)
+              : launch_t<2, false, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+                                                   st, why);
+}
+
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, bool weights_static,
-                          cudaStream_t st, const char** why, const ArParams* ar_in) {
+                          const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws,
+                          bool weights_static, cudaStream_t st, const char** why, const ArParams* ar_in) {
   const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
+  if (group == 64)
+    return launch_small_group<64>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+  if (group == 32)
+    return launch_small_group<32>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
 #ifdef SQ_DEC_M1_SLOT3
   // experiment: M = 1 with the 74-KB three-CTA configuration but only two CTAs per SM, so
   // the next kernel's first CTAs can become resident (and stream their weights) in the

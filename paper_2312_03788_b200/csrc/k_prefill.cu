@@ -50,7 +50,7 @@ constexpr int kAFullCount = kStageSplit ? kDQW / 2 : kDQW;
 
 constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
 constexpr int C_STAGE_BYTES = BM * (kGroup / 2);  // 8 KB
-constexpr int SZ_BYTES = BM * 2;                  // 256 B
+constexpr int SZ_BYTES = 4 * BM * 2;              // Δ (or Z) rows of one 128-k stage: [128 / GS][BM] fp16, GS >= 32
 
 constexpr int OFF_X = 0;
 constexpr int OFF_C = OFF_X + NSX * X_STAGE_BYTES;
@@ -279,7 +279,7 @@ struct PSched {
   }
 };
 
-template <bool kBF16>
+template <bool kBF16, int GS>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
@@ -362,10 +362,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const int n0 = (tile / m_tiles) * BM;
         for (int g = sc.g0; g < sc.g1; ++g) {
           mbar_wait(c_empty(cs), cph ^ 1);
-          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SZ_BYTES);
+          constexpr int SUB = kGroup / GS;  // quantization groups per 128-k stage
+          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SUB * BM * 2);
           tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
-          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g);
-          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g);
+          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g * SUB);
+          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g * SUB);
           if (++cs == NSC) { cs = 0; cph ^= 1; }
         }
       }
@@ -409,107 +410,66 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     const int ch = (warp - kDequantWarp0) / 4;  // column split among warps of one quarter
     const int row = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    int cs = 0, as = 0;
-    uint32_t cph = 0, aph = 0, dph = 0;
-    int ai = 0;  // A-ring stage counter (stage-split mode)
+    int cs = 0;
+    uint32_t cph = 0, dph = 0;
+    int ai = 0;  // A-ring stage counter
     for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
       const int tile = sc.tile;
       const int n0 = (tile / m_tiles) * BM;
       const int m0 = (tile % m_tiles) * BT;
       for (int g = sc.g0; g < sc.g1; ++g) {
-        if constexpr (kStageSplit) {
-          mbar_wait(c_full(cs), cph);
-          const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
-          const int sw = (row >> 1) & 3;  // SWIZZLE_64B: chunk c sits at c ^ ((row >> 1) & 3)
-          const uint4 c0v = *reinterpret_cast<const uint4*>(crow + (((2 * ch) ^ sw) << 4));
-          const uint4 c1v = *reinterpret_cast<const uint4*>(crow + (((2 * ch + 1) ^ sw) << 4));
-          const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
-          const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(c_empty(cs));
-          if (++cs == NSC) { cs = 0; cph ^= 1; }
-          const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), __ushort_as_half(zbits)));
-          const __half2 d2h = __half2half2(__ushort_as_half(sbits));
-          const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
-          const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
-          const float df = __half2float(__ushort_as_half(sbits));
-          const uint32_t words[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
-          uint32_t a[32];
-if (!kBF16 && df > 4366.0f) {
-#pragma unroll
-            for (int wd = 0; wd < 8; ++wd) dequant8<kBF16, true>(words[wd], zc, d2, df, &a[4 * wd]);
-          } else {
-#pragma unroll
-            for (int wd = 0; wd < 8; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
-          }
-          // this warp's stage: k-half ch of the group -> A-ring index ai + ch
-          const int i = ai + ch;
-          const int slot = i % NSA;
-          mbar_wait(a_empty(slot), ((i / NSA) & 1) ^ 1);
-          tc_fence_after();
-          tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)slot * (BK / 2), a);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(a_full(slot));
-          ai += 2;
-          continue;
-        }
+        // the two warps of a lane quarter take alternate 64-k halves of each 128-k stage, so
+        // two A stages are in flight at once and the tcgen05.st -> wait::st -> arrive latency
+        // of one overlaps the other's math
+        static_assert(kStageSplit, "two dequant warps per TMEM lane quarter");
         mbar_wait(c_full(cs), cph);
         const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
-        // SWIZZLE_64B: 16-byte chunk c of this row sits at chunk c ^ ((row >> 1) & 3)
-        const int sw = (row >> 1) & 3;
-        // this warp's 16-byte chunks of the group row: k-block h uses chunks 2h .. 2h+1,
-        // split across the kColSplit warps of this lane quarter
-        constexpr int kCh = 4 / kColSplit;
-        uint4 cv[kCh];
+        const int sw = (row >> 1) & 3;  // SWIZZLE_64B: chunk c sits at c ^ ((row >> 1) & 3)
+        const uint4 c0v = *reinterpret_cast<const uint4*>(crow + (((2 * ch) ^ sw) << 4));
+        const uint4 c1v = *reinterpret_cast<const uint4*>(crow + (((2 * ch + 1) ^ sw) << 4));
+        // quantization groups of this warp's 64 k: one (GS >= 64) or two (GS = 32)
+        constexpr int NG = GS >= 64 ? 1 : 2;
+        uint16_t sbits[NG], zbits[NG];
 #pragma unroll
-        for (int c = 0; c < kCh; ++c) {
-          const int cc = (c / (2 / kColSplit)) * 2 + (kColSplit == 2 ? ch : (c % 2));
-          cv[c] = *reinterpret_cast<const uint4*>(crow + ((cc ^ sw) << 4));
+        for (int h = 0; h < NG; ++h) {
+          const int sub = (64 * ch + 32 * h) / GS;
+          sbits[h] = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + (sub * BM + row) * 2);
+          zbits[h] = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + (sub * BM + row) * 2);
         }
-        const uint16_t sbits = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + row * 2);
-        const uint16_t zbits = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + row * 2);
         __syncwarp();
         if (lane == 0) mbar_arrive(c_empty(cs));
         if (++cs == NSC) { cs = 0; cph ^= 1; }
-
-        const __half zh = __ushort_as_half(zbits);
-        const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), zh));
-        const __half2 d2h = __half2half2(__ushort_as_half(sbits));
-        const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
-        const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
-        const float df = __half2float(__ushort_as_half(sbits));
+        const uint32_t words[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
+        uint32_t a[32];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // two 64-k stages per group
-          constexpr int kW = 8 / kColSplit;  // 32-bit code words of this warp per k-block
-          uint32_t words[kW];
+        for (int h = 0; h < NG; ++h) {
+          const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), __ushort_as_half(zbits[h])));
+          const __half2 d2h = __half2half2(__ushort_as_half(sbits[h]));
+          const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
+          const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
+          const float df = __half2float(__ushort_as_half(sbits[h]));
+          constexpr int WPG = 8 / NG;  // code words per group
+          if (!kBF16 && df > 4366.0f) {
 #pragma unroll
-          for (int c = 0; c < kW / 4; ++c) {
-            const uint4 v = cv[h * (kW / 4) + c];
-            words[4 * c] = v.x; words[4 * c + 1] = v.y; words[4 * c + 2] = v.z; words[4 * c + 3] = v.w;
-          }
-          uint32_t a[4 * kW];
-if (!kBF16 && df > 4366.0f) {
-#pragma unroll
-            for (int wd = 0; wd < kW; ++wd) dequant8<kBF16, true>(words[wd], zc, d2, df, &a[4 * wd]);
+            for (int wd = 0; wd < WPG; ++wd)
+              dequant8<kBF16, true>(words[h * WPG + wd], zc, d2, df, &a[4 * (h * WPG + wd)]);
           } else {
 #pragma unroll
-            for (int wd = 0; wd < kW; ++wd) dequant8<kBF16>(words[wd], zc, d2, df, &a[4 * wd]);
+            for (int wd = 0; wd < WPG; ++wd)
+              dequant8<kBF16>(words[h * WPG + wd], zc, d2, df, &a[4 * (h * WPG + wd)]);
           }
-          mbar_wait(a_empty(as), aph ^ 1);
-          tc_fence_after();
-          if constexpr (kColSplit == 1)
-            tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2),
-                               *reinterpret_cast<const uint32_t(*)[32]>(a));
-          else
-            tmem_st_32x32b_x16(tmem_base + lane_addr + A_COL + (uint32_t)as * (BK / 2) + ch * 16, a);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(a_full(as));
-          if (++as == NSA) { as = 0; aph ^= 1; }
         }
+        // this warp's stage: k-half ch of the group -> A-ring index ai + ch
+        const int i = ai + ch;
+        const int slot = i % NSA;
+        mbar_wait(a_empty(slot), ((i / NSA) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)slot * (BK / 2), a);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(slot));
+        ai += 2;
       }
       // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
       pdl_wait();  // (returns at once after the first tile) Y may be read by the previous kernel
@@ -647,7 +607,7 @@ size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 }
 
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, size_t,
+                           const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws, size_t,
                            bool weights_static, cudaStream_t st, const char** why) {
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = K / kGroup;
@@ -658,10 +618,11 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
                       (uint64_t)K * 2, BK, x_rows, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
                        (uint64_t)K / 2, kGroup / 2, BM, CU_TENSOR_MAP_SWIZZLE_64B);
-  ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G,
-                       (uint64_t)N * 2, BM, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
-  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)G,
-                       (uint64_t)N * 2, BM, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const int sub = kGroup / group;  // scale / zero rows per 128-k stage
+  ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G * sub,
+                       (uint64_t)N * 2, BM, sub, CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)G * sub,
+                       (uint64_t)N * 2, BM, sub, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!ok) {
     *why = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
@@ -673,7 +634,10 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
   const int cta_q = units / grid, cta_r = units % grid;
   float* partials = reinterpret_cast<float*>(ws);
   int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
-  auto kern = x_dtype == SQ_BF16 ? prefill_kernel<true> : prefill_kernel<false>;
+  auto kern = x_dtype == SQ_BF16 ? (group == 32 ? prefill_kernel<true, 32> : group == 64 ? prefill_kernel<true, 64>
+                                                                                       : prefill_kernel<true, 128>)
+                                  : (group == 32 ? prefill_kernel<false, 32> : group == 64 ? prefill_kernel<false, 64>
+                                                                                        : prefill_kernel<false, 128>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

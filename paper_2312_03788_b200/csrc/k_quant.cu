@@ -6,9 +6,11 @@
 //       pack: low nibble = even k
 //
 // Layout: a CTA of 256 threads owns 32 consecutive output channels (rows n) and
-// kGroupsPerCta consecutive groups; 8 lanes share one (row, group): lane `sub`
-// holds elements [16*sub, 16*sub+16) of the group (two 16-byte loads, all issued
-// before any arithmetic).  Min/max are reduced with half2 min/max + 3 xor-shuffles.
+// kSlotsPerCta consecutive 128-k slots; 8 lanes share one (row, slot): lane `sub` holds
+// elements [16*sub, 16*sub+16) of the slot (two 16-byte loads, all issued before any
+// arithmetic).  A group ("different group sizes": GS = 128, 64 or 32) is
+// GS/16 consecutive lanes; min/max are reduced with half2 min/max + log2(GS/16)
+// xor-shuffles.
 //
 // Exactness:
 //  * fold: fp32 multiply rounded toward zero + FMA residual gives the product
@@ -31,9 +33,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kRowsPerCta = 32;
-constexpr int kLanesPerGroup = 8;
-constexpr int kGroup = 128;
-constexpr int kGroupsPerCta = 4;
+constexpr int kLanesPerSlot = 8;
+constexpr int kSlot = 128;      // k per slot; K % 128 == 0 for every group size
+constexpr int kSlotsPerCta = 4;
 
 template <bool kBF16>
 struct Fmt;
@@ -93,23 +95,24 @@ __device__ __forceinline__ float rha_div_f16(float v, float d, float inv) {
   return __fmaf_rn(-(c + h), d, v) == 0.0f ? c + 2.0f * h : c;
 }
 
-template <bool kBF16>
+template <bool kBF16, int GS>
 __global__ void __launch_bounds__(kThreads)
-quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int N, int K, int G,
+quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int N, int K, int NSL,
                 uint8_t* __restrict__ Wq, uint16_t* __restrict__ scales,
                 uint16_t* __restrict__ zeros, int* __restrict__ nonfinite) {
-  const int sub = threadIdx.x % kLanesPerGroup;
-  const int n = blockIdx.y * kRowsPerCta + threadIdx.x / kLanesPerGroup;
-  const int g0 = blockIdx.x * kGroupsPerCta;
+  constexpr int kLanesPerGroup = GS / 16;
+  const int sub = threadIdx.x % kLanesPerSlot;
+  const int n = blockIdx.y * kRowsPerCta + threadIdx.x / kLanesPerSlot;
+  const int g0 = blockIdx.x * kSlotsPerCta;  // first slot of the CTA
   const bool row_ok = n < N;
 
   // issue every load of the CTA's groups first (memory-level parallelism)
-  uint4 va[kGroupsPerCta], vb[kGroupsPerCta];
+  uint4 va[kSlotsPerCta], vb[kSlotsPerCta];
 #pragma unroll
-  for (int j = 0; j < kGroupsPerCta; ++j) {
+  for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
-    if (row_ok && g < G) {
-      const uint16_t* p = W + (size_t)n * K + (size_t)g * kGroup + sub * 16;
+    if (row_ok && g < NSL) {
+      const uint16_t* p = W + (size_t)n * K + (size_t)g * kSlot + sub * 16;
       va[j] = ld_nc_v4(p);
       vb[j] = ld_nc_v4(p + 8);
     } else {
@@ -119,12 +122,12 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
   }
 
 #pragma unroll
-  for (int j = 0; j < kGroupsPerCta; ++j) {
+  for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
-    if (g >= G) break;  // uniform across the CTA
+    if (g >= NSL) break;  // uniform across the CTA
     uint32_t w[8] = {va[j].x, va[j].y, va[j].z, va[j].w, vb[j].x, vb[j].y, vb[j].z, vb[j].w};
     if (s != nullptr) {
-      const float4* sp = reinterpret_cast<const float4*>(s + (size_t)g * kGroup + sub * 16);
+      const float4* sp = reinterpret_cast<const float4*>(s + (size_t)g * kSlot + sub * 16);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float4 sv = __ldg(sp + q);
@@ -190,11 +193,12 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
       }
     }
     if (row_ok) {
-      *reinterpret_cast<uint2*>(Wq + (size_t)n * (K / 2) + (size_t)g * (kGroup / 2) + sub * 8) =
+      *reinterpret_cast<uint2*>(Wq + (size_t)n * (K / 2) + (size_t)g * (kSlot / 2) + sub * 8) =
           make_uint2(packed[0], packed[1]);
-      if (sub == 0) {
-        scales[(size_t)g * N + n] = nf ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(d));
-        zeros[(size_t)g * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
+      if (sub % kLanesPerGroup == 0) {  // first lane of each group
+        const size_t gi = (size_t)g * (kSlot / GS) + sub / kLanesPerGroup;
+        scales[gi * N + n] = nf ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(d));
+        zeros[gi * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
         if (nf && nonfinite != nullptr) atomicAdd(nonfinite, 1);
       }
     }
@@ -203,18 +207,28 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
 
 }  // namespace
 
-cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K,
+template <int GS>
+void launch_gs(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, uint8_t* Wq, uint16_t* scales,
+               uint16_t* zeros, int* nonfinite, cudaStream_t st) {
+  const int NSL = (int)(K / kSlot);
+  dim3 grid((unsigned)((NSL + kSlotsPerCta - 1) / kSlotsPerCta), (unsigned)((N + kRowsPerCta - 1) / kRowsPerCta));
+  if (w_dtype == SQ_BF16)
+    quantize_kernel<true, GS><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, NSL, Wq, scales,
+                                                         zeros, nonfinite);
+  else
+    quantize_kernel<false, GS><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, NSL, Wq, scales,
+                                                          zeros, nonfinite);
+}
+
+cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, int group,
                             uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
                             cudaStream_t st) {
-  const int G = (int)(K / kGroup);
-  dim3 grid((unsigned)((G + kGroupsPerCta - 1) / kGroupsPerCta),
-            (unsigned)((N + kRowsPerCta - 1) / kRowsPerCta));
-  if (w_dtype == SQ_BF16)
-    quantize_kernel<true><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, G, Wq,
-                                                     scales, zeros, nonfinite);
+  if (group == 32)
+    launch_gs<32>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
+  else if (group == 64)
+    launch_gs<64>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
   else
-    quantize_kernel<false><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, G, Wq,
-                                                      scales, zeros, nonfinite);
+    launch_gs<128>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,8 @@ static sq_status cuda_status(cudaError_t e, const char* where) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static bool valid_dtype(int d) { return d == SQ_F16 || d == SQ_BF16; }
+// PAPER.md:160 "Group-size is usually set to be 128"; "different group sizes"
+static bool valid_group(int g) { return g == 128 || g == 64 || g == 32; }
 
 int num_sms() {
   int dev = 0;
@@ -172,13 +174,13 @@ sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s,
   g_last_error.clear();
   if (!W || !Wq || !scales || !zeros) return fail(SQ_ERR_NULL, "sq_quantize_pack_groupwise: null pointer");
   if (N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: N=%lld K=%lld", (long long)N, (long long)K);
-  if (group != 128 || K % group != 0 || !valid_dtype(w_dtype))
+  if (!valid_group(group) || K % 128 != 0 || !valid_dtype(w_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_quantize_pack_groupwise: group=%d K=%lld dtype=%d", group, (long long)K, w_dtype);
   if (N % 8 != 0 || !aligned16(W) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
       (s && !aligned16(s)))
     return fail(SQ_ERR_ALIGN, "sq_quantize_pack_groupwise: N %% 8 != 0 or unaligned pointer");
   if (N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: too large");
-  return cuda_status(launch_quantize(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite_count,
+  return cuda_status(launch_quantize(W, w_dtype, s, N, K, group, Wq, scales, zeros, nonfinite_count,
                                      (cudaStream_t)stream), "quantize");
 }
 
@@ -203,7 +205,7 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
   if (M == 0 && N > 0 && K > 0) return SQ_OK;  // no-op; X/Y may be empty (null) tensors
   if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm: null pointer");
   if (M < 0 || N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
-  if (group != 128 || K % group != 0 || !valid_dtype(x_dtype))
+  if (!valid_group(group) || K % 128 != 0 || !valid_dtype(x_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
   if (flags & ~(unsigned)SQ_GEMM_WEIGHTS_STATIC) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: flags 0x%x", flags);
   if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
@@ -219,13 +221,14 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
     if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: decode needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
-    cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, wstatic, st, &why);
+    cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group, workspace, wstatic,
+                                  st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
     return cuda_status(e, "decode");
   }
   if (path == SQ_PATH_DECODE_TC) {
-    if (M > kDecodeTcMaxM)
-      return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: tcgen05 decode path needs M <= %d", kDecodeTcMaxM);
+    if (M > kDecodeTcMaxM || group != 128)
+      return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: tcgen05 decode path needs M <= %d and group 128", kDecodeTcMaxM);
     const size_t need = dtc_workspace_bytes(N);
     if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: tcgen05 decode needs %zu workspace bytes (16-byte aligned)", need);
@@ -239,7 +242,7 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
     if (need > 0 && (workspace == nullptr || workspace_bytes < need || !aligned16(workspace)))
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
-    cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K,
+    cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group,
                                    workspace, workspace_bytes, wstatic, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm prefill: %s", why);
     return cuda_status(e, "prefill");
@@ -331,7 +334,7 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
   // decode: one kernel -- the epilogue pushes each finished row block to every rank and
   // reduces its own row blocks once every rank's copy has arrived
   if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm_allreduce: null pointer");
-  if (K <= 0 || group != 128 || K % group != 0 || !valid_dtype(x_dtype))
+  if (K <= 0 || !valid_group(group) || K % 128 != 0 || !valid_dtype(x_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
   if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) || !aligned16(Y))
     return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: N %% 8 != 0 or unaligned pointer");
@@ -340,7 +343,7 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
     return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm_allreduce: decode needs %zu workspace bytes", need);
   const ArParams ar{reinterpret_cast<uint8_t* const*>(peer_bufs), n_max, error_flag, rank, world, epoch};
   const char* why = nullptr;
-  cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace,
+  cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group, workspace,
                                 (flags & SQ_GEMM_WEIGHTS_STATIC) != 0, (cudaStream_t)stream, &why, &ar);
   if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: %s", why);
   return cuda_status(e, "sq_w4a16_gemm_allreduce");

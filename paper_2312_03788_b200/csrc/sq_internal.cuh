@@ -15,7 +15,8 @@ cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K,
                              float* out_bits_as_float, cudaStream_t st);
 cudaError_t launch_smooth_finalize(const float* act_max, float* s_inout, int64_t K,
                                    double alpha, double eps, cudaStream_t st);
-cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K,
+// group: 32, 64 or 128 (K % 128 == 0)
+cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, int group,
                             uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
                             cudaStream_t st);
 
@@ -45,8 +46,8 @@ struct ArParams {
 // written by the preceding kernels, so with PDL the weight loads may start before the
 // previous kernel has finished.
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, bool weights_static,
-                          cudaStream_t st, const char** why, const ArParams* ar = nullptr);
+                          const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws,
+                          bool weights_static, cudaStream_t st, const char** why, const ArParams* ar = nullptr);
 
 // tcgen05 decode for 9 <= M <= 64 (k_dtc.cu)
 size_t dtc_partials_bytes();
@@ -56,7 +57,7 @@ cudaError_t launch_dtc(const void* X, int x_dtype, const uint8_t* Wq, const uint
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K,
+                           const uint16_t* zeros, void* Y, int M, int N, int K, int group,
                            void* workspace, size_t ws_bytes, bool weights_static, cudaStream_t st,
                            const char** why);
 

@@ -57,7 +57,9 @@ def test_gemm_argument_errors(L):
     assert _gemm(L, M=-1) == sq.SQ_ERR_SHAPE
     assert _gemm(L, N=0) == sq.SQ_ERR_SHAPE
     assert _gemm(L, K=0) == sq.SQ_ERR_SHAPE
-    assert _gemm(L, g=64) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, g=16) == sq.SQ_ERR_UNSUPPORTED      # group sizes: 32, 64, 128
+    assert _gemm(L, g=256) == sq.SQ_ERR_UNSUPPORTED
+    assert _gemm(L, g=64, K=192) == sq.SQ_ERR_UNSUPPORTED   # K % 128 != 0 for every group size
     assert _gemm(L, K=200) == sq.SQ_ERR_UNSUPPORTED
     assert _gemm(L, dt=7) == sq.SQ_ERR_UNSUPPORTED
     assert _gemm(L, N=252) == sq.SQ_ERR_ALIGN
@@ -73,7 +75,8 @@ def test_quantize_argument_errors(L):
     assert q(None, 0, None, 8, 128, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_NULL
     assert q(FAKE, 0, None, 0, 128, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_SHAPE
     assert q(FAKE, 0, None, 8, 130, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
-    assert q(FAKE, 0, None, 8, 256, 32, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
+    assert q(FAKE, 0, None, 8, 256, 16, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
+    assert q(FAKE, 0, None, 8, 96, 32, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
     assert q(FAKE, 3, None, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
     assert q(FAKE, 0, None, 12, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
     assert q(FAKE, 0, FAKE_MIS, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
@@ -163,7 +166,7 @@ def test_gemm_allreduce_argument_errors(L):
     assert call(peers=None) == sq.SQ_ERR_NULL
     assert call(err=None) == sq.SQ_ERR_NULL
     assert call(n_max=1028) == sq.SQ_ERR_ALIGN
-    assert call(g=64) == sq.SQ_ERR_UNSUPPORTED
+    assert call(g=16) == sq.SQ_ERR_UNSUPPORTED
     assert call(flags=2) == sq.SQ_ERR_UNSUPPORTED   # unknown flag bit
     assert call(M=0) == sq.SQ_OK
 

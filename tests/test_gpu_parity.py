@@ -85,8 +85,8 @@ def test_smooth_scales(alpha, N, K):
 
 
 # ------------------------------------------------------------------ a3/a4
-def _check_quant(W_np, s_np, q: sq.QuantizedLinear, w_dtype="f16", nonfinite=None):
-    ref = oracle.quantize_pack(W_np, s_np, 128, w_dtype)
+def _check_quant(W_np, s_np, q: sq.QuantizedLinear, w_dtype="f16", nonfinite=None, group=128):
+    ref = oracle.quantize_pack(W_np, s_np, group, w_dtype)
     assert (q.Wq.cpu().numpy() == ref["Wq"]).all()
     assert (_bits16(q.scales) == ref["scales"]).all()
     assert (_bits16(q.zeros) == ref["zeros"]).all()
@@ -159,15 +159,15 @@ class GemmCase:
         return err
 
 
-def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0):
+def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0, group=128):
     if W is None:
         W = synth.weights(N, K, seed=seed + 100, heavy=True)
     s = None
     if smooth:
         am = oracle.act_absmax(synth.activations(2048, K, seed=seed + 200).astype(np.float16))
         s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
-    ref_q = oracle.quantize_pack(W, s, 128)
-    q = sq.quantize_pack_groupwise(_t(W), None if s is None else _t(s))
+    ref_q = oracle.quantize_pack(W, s, group)
+    q = sq.quantize_pack_groupwise(_t(W), None if s is None else _t(s), group=group)
     X = synth.activations(M, K, seed=seed + 300, outlier_seed=seed + 200) * x_scale
     if s is not None:  # a5: X̂ = X diag(s)^-1, rounded once to the activation dtype
         X = X.astype(np.float64) / s.astype(np.float64)[None, :]
@@ -179,8 +179,8 @@ def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0):
     y = sq.w4a16_gemm(x, q, workspace=ws, path=path)
     torch.cuda.synchronize()
     xn, xd = _x_np_for(x)
-    y_ref = oracle.gemm(xn, ref_q["Wq"], ref_q["scales"], ref_q["zeros"], 128, xd)
-    W_hat = oracle.dequant(ref_q["Wq"], ref_q["scales"], ref_q["zeros"], 128)
+    y_ref = oracle.gemm(xn, ref_q["Wq"], ref_q["scales"], ref_q["zeros"], group, xd)
+    W_hat = oracle.dequant(ref_q["Wq"], ref_q["scales"], ref_q["zeros"], group)
     x64 = x.float().cpu().double().numpy()
     return GemmCase(y, y_ref, x64, W_hat, xd)
 
@@ -386,3 +386,40 @@ def test_gemm_decode_tc_parity(M, N, K, dtype):
         ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE_TC) for _ in range(3)]
         torch.cuda.synchronize()
         assert all(torch.equal(ys[0], yy) for yy in ys[1:])
+
+
+# ------------------------------------------------------------------ N3: group sizes 64 / 32
+@pytest.mark.parametrize("group", [32, 64])
+@pytest.mark.parametrize("N,K", [(264, 384), (512, 1024)])
+def test_quantize_group_sizes_bitexact(group, N, K):
+    """PAPER.md:185 "different group sizes": codes, Δ and Z bit-exact with the oracle at
+    g = 32 / 64, with the smoothing fold, on edge groups and on bf16 weights."""
+    W = synth.weights(N, K, seed=group + N, heavy=True)
+    am = oracle.act_absmax(synth.activations(512, K, seed=K).astype(np.float16))
+    s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
+    nf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    q = sq.quantize_pack_groupwise(_t(W), _t(s), group=group, nonfinite=nf)
+    assert q.scales.shape == (K // group, N)
+    _check_quant(W, s, q, nonfinite=nf, group=group)
+    E = synth.edge_groups(group, seed=group)
+    pad = (-E.shape[0]) % 8
+    We = np.concatenate([E, synth.weights(pad, group, seed=6)]).astype(np.float16)
+    We = np.tile(We, (1, 128 // group))                       # K = 128: 128 / group groups per row
+    nf.zero_()
+    qe = sq.quantize_pack_groupwise(_t(We), group=group, nonfinite=nf)
+    _check_quant(We, None, qe, nonfinite=nf, group=group)
+    Wb = torch.from_numpy(W.astype(np.float32)).to(torch.bfloat16)
+    qb = sq.quantize_pack_groupwise(Wb.to(DEV), _t(s), group=group)
+    _check_quant(Wb.view(torch.int16).numpy().view(np.uint16), s, qb, w_dtype="bf16", group=group)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("group", [32, 64])
+@pytest.mark.parametrize("path,M", [(sq.SQ_PATH_DECODE, 1), (sq.SQ_PATH_DECODE, 5), (sq.SQ_PATH_DECODE, 16),
+                                    (sq.SQ_PATH_PREFILL, 17), (sq.SQ_PATH_PREFILL, 300)])
+@pytest.mark.parametrize("N,K", [(264, 1152), (2048, 4096)])
+def test_gemm_group_sizes_parity(path, M, N, K, group, dtype):
+    """W4A16 GEMM at g = 32 / 64 through both paths (decode feeds RN((q - Z)Δ) operands to
+    mma.sync, prefill to tcgen05), ragged row blocks and 128-k stages, stream-K fixups,
+    against the oracle element by element."""
+    _gemm_case(M, N, K, dtype, path, seed=M + group, group=group).check(dtype)

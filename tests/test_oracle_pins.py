@@ -525,3 +525,60 @@ def test_rn_bf16_bits_against_exact():
     sp = oracle.rn_bf16_bits(np.array([0.0, -0.0, np.inf, -np.inf, np.nan]))
     assert [int(v) for v in sp[:4]] == [0x0000, 0x8000, 0x7F80, 0xFF80]
     assert (int(sp[4]) & 0x7F80) == 0x7F80 and (int(sp[4]) & 0x007F) != 0
+
+
+@pytest.mark.parametrize("group", [32, 64])
+def test_n3_group_sizes_match_groupwise_loop(group):
+    """N3 (PAPER.md:185 "Support group-wise quantization for different group sizes"):
+    quantize_pack with g = 32 / 64 equals the exact-rational Eq. 1 quantizer applied to every
+    (n, group of g consecutive k) (readings S1-S4, S6), including the smoothing fold; codes,
+    Δ bits and Z are identical, and dequant reconstructs (q - Z)·Δ per group."""
+    g = synth.rng(70 + group)
+    N, K = 5, 256
+    W = synth.weights(N, K, seed=71, heavy=True)
+    s = g.uniform(0.1, 10, size=K).astype(np.float32)
+    q = oracle.quantize_pack(W, s, group)
+    assert q["scales"].shape == (K // group, N)
+    for n in range(N):
+        for gi in range(K // group):
+            v = [float(np.float16(float(W[n, k]) * float(s[k]))) for k in range(gi * group, (gi + 1) * group)]
+            c, d, z = ex.quantize_group(v)
+            assert q["codes"][n, gi * group:(gi + 1) * group].tolist() == c
+            assert Fraction(float(np.uint16(q["scales"][gi, n]).view(np.float16))) == d
+            assert float(np.uint16(q["zeros"][gi, n]).view(np.float16)) == z
+    What = oracle.dequant(q["Wq"], q["scales"], q["zeros"], group)
+    codes = oracle.unpack_nibbles(q["Wq"])
+    for n in range(N):
+        for k in (0, group - 1, group, K - 1):
+            gi = k // group
+            d = float(np.uint16(q["scales"][gi, n]).view(np.float16))
+            z = float(np.uint16(q["zeros"][gi, n]).view(np.float16))
+            assert What[n, k] == (codes[n, k] - z) * d
+
+
+@pytest.mark.parametrize("group", [32, 64])
+def test_n3_group_sizes_idempotence_and_bound(group):
+    """P8 and P10 at g = 32 / 64: Q(D(Q(W))) == Q(W) for zero-straddling groups and every
+    element within Δ/2 (+ the 2^-24 floor excess) of its reconstruction."""
+    W = synth.weights(64, 512, seed=72)
+    q = oracle.quantize_pack(W, None, group)
+    What = oracle.dequant(q["Wq"], q["scales"], q["zeros"], group)
+    codes = q["codes"].reshape(-1, group)
+    for i, grp in enumerate(What.reshape(-1, group)[::7]):   # every 7th group: D exact in fp64
+        c2, _, _ = oracle.quantize_group(grp)
+        assert c2 == codes[7 * i].tolist()
+    v = W.astype(np.float64).reshape(-1, group)
+    r = v.max(axis=1) - v.min(axis=1)
+    d = q["delta"].T.reshape(-1)
+    err = np.abs(v - What.reshape(-1, group)).max(axis=1)
+    assert (err <= d / 2 + np.maximum(0.0, r - 15 * d) + 1e-12).all()
+
+
+def test_n3_footprint_by_group_size():
+    """P12 generalised: bytes / fp16 bytes = (0.5 + 4/g) / 2: 0.265625 (g = 128),
+    0.28125 (64), 0.3125 (32), measured on the layout the quantizer writes."""
+    for group, want in ((128, 0.265625), (64, 0.28125), (32, 0.3125)):
+        assert oracle.footprint_ratio(64, 512, group) == want
+        q = oracle.quantize_pack(synth.weights(64, 512, seed=73), None, group)
+        nbytes = q["Wq"].nbytes + q["scales"].nbytes + q["zeros"].nbytes
+        assert nbytes / (2.0 * 64 * 512) == want
