@@ -18,10 +18,11 @@
 //    correctly rounded exact product (one rounding, reading S13).
 //  * r = hi - lo in fp64 (exact for fp16 inputs), Δ = RZ16(r/15) via fp64 division
 //    then RZ->fp32->RZ->fp16 (RZ∘RZ = RZ).
-//  * codes (fp16 path): t = v * RN(1/Δ) has |error| <= 2^-19 for |t| < 16 while a
-//    non-tie v/Δ is >= 2^-12 from any half-integer (fp16 v, Δ), so trunc(t ± 1/2) is the
-//    RHA of v/Δ except at an exact tie that t missed, which one branch-free FMA detects
-//    exactly (v - (c ± 1/2)Δ is computed exactly) and moves away from zero.
+//  * codes (fp16 path): a non-tie v/Δ is >= 2^-12 from any half-integer (fp16 v, Δ), so
+//    rounding v * RN(1/Δ)(1 + 2^-17) to the nearest integer (one FFMA with the 1.5 * 2^23
+//    magic constant) is RHA(v/Δ): the factor pushes exact ties away from zero by more than
+//    the product's error and moves non-ties by less than the gap (see the code).  The
+//    clamp and the nibble packing then run on two codes per instruction (s16x2).
 //  * codes (bf16 path): the gap can be as small as 2^-20, so v/Δ uses fp64 division.
 #include <algorithm>
 
@@ -80,19 +81,6 @@ __device__ __forceinline__ uint16_t fold1(uint16_t wbits, float s) {
   const float e = __fmaf_rn(w, s, -p);
   if (e != 0.0f) p = __uint_as_float(__float_as_uint(p) | 1u);
   return Fmt<kBF16>::from_f_rn(p);
-}
-
-// RHA(v / d) for fp16 v, d (see header comment), as float, branch-free.  t = v * RN(1/d)
-// is within 2^-19 of x = v/d (|x| < 16) while a non-tie x is >= 2^-12 from every k + 1/2,
-// so c = trunc(t + copysign(1/2, t)) is RHA(x) unless x is an exact tie that t missed by
-// rounding toward zero; then v - (c + copysign(1/2, t)) d is exactly 0 (one FMA, the
-// product is exact) and c moves one step away from zero.  A nonzero exact difference
-// never rounds to 0, so non-ties are never moved.
-__device__ __forceinline__ float rha_div_f16(float v, float d, float inv) {
-  const float t = v * inv;
-  const float h = copysignf(0.5f, t);
-  const float c = truncf(t + h);
-  return __fmaf_rn(-(c + h), d, v) == 0.0f ? c + 2.0f * h : c;
 }
 
 template <bool kBF16, int GS>
@@ -169,27 +157,51 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
       d = (lo == 0.0f) ? 1.0f : fabsf(lo);
     }
     if (nf) d = 1.0f;
-    // Z (reading S2), once per group: fp64 division (exact-enough for bf16 lo too)
-    const float z = (float)fmin(fmax(round(-(double)lo / (double)d), 0.0), 15.0);
+    // fp16: RN(1/Δ)(1 + 2^-17) turns RHA(v / Δ) into one FFMA (see the codes below)
+    const float inv = kBF16 ? 0.0f : __fmul_rn(__frcp_rn(d), 1.0f + 0x1p-17f);
+    // Z = clamp(RHA(-lo / Δ), 0, 15) (reading S2): for fp16 the same exact one-FFMA rounding
+    // (-lo is an fp16 value); bf16 lo needs the fp64 quotient
+    float z;
+    if (!kBF16) {
+      const int zc = __float_as_int(__fmaf_rn(-lo, inv, 12582912.0f)) - 0x4B400000;
+      z = (float)min(max(zc, 0), 15);
+    } else {
+      z = (float)fmin(fmax(round(-(double)lo / (double)d), 0.0), 15.0);
+    }
 
     // codes for this lane's 16 elements, packed low nibble = even k
     uint32_t packed[2] = {0u, 0u};
     if (!nf) {
-      const float inv = __frcp_rn(d);
+      if (!kBF16) {
+        // RHA(v / Δ) as ONE FFMA per element: RN(v * inv' + 1.5 * 2^23) - 1.5 * 2^23 with
+        // inv' = RN(RN(1/Δ) (1 + 2^-17)).  v * inv' = x (1 + 2^-17)(1 + δ), |δ| <= 3 * 2^-24,
+        // x = v / Δ.  An exact tie x = k + 1/2 is pushed away from zero by |x| 2^-17, far
+        // more than |x| δ, so round-to-nearest of it is RHA; a non-tie (|x| < 16) lies
+        // >= 2^-12 from every half-integer (fp16 v and Δ), and |x| (2^-17 + 3 * 2^-24) <
+        // 2^-12 cannot cross one.  |x| >= 16 is clamped below whichever way it rounds, and
+        // |x| < 2^15 - 16 always (Δ >= (r / 15)(1 - 2^-10) and r >= |v| 2^-11), so the
+        // integer c + Z fits the signed 16-bit lanes of the clamp.
+        const int zoff = (int)z - 0x4B400000;  // + Z, - the bits of 1.5 * 2^23
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t bits = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
-        const float v = Fmt<kBF16>::to_f((uint16_t)bits);
-        float c;
-        if (kBF16) {
-          c = (float)round((double)v / (double)d);
-        } else {
-          c = rha_div_f16(v, d, inv);
+        for (int q = 0; q < 8; ++q) {  // element pair (2q, 2q + 1) = the two halves of w[q]
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+          const int c0 = __float_as_int(__fmaf_rn(f.x, inv, 12582912.0f)) + zoff;
+          const int c1 = __float_as_int(__fmaf_rn(f.y, inv, 12582912.0f)) + zoff;
+          uint32_t cc = __byte_perm((uint32_t)c0, (uint32_t)c1, 0x5410);  // (c0, c1) as s16x2
+          asm("max.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0u));
+          asm("min.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0x000F000Fu));
+          const uint32_t byte = (cc & 0xFu) | ((cc >> 12) & 0xF0u);    // low nibble = even k
+          packed[q >> 2] += byte << (8 * (q & 3));
         }
-        c = fminf(fmaxf(c + z, 0.0f), 15.0f);
-        // integral c in [0, 15]: c + 2^23 is exact and its low mantissa bits are c (no
-        // float->int conversion instruction)
-        packed[i >> 3] |= (__float_as_uint(c + 8388608.0f) & 0xFu) << (4 * (i & 7));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t bits = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
+          const float v = Fmt<kBF16>::to_f((uint16_t)bits);
+          float c = (float)round((double)v / (double)d);  // bf16: the gap can be 2^-20, fp64
+          c = fminf(fmaxf(c + z, 0.0f), 15.0f);
+          packed[i >> 3] |= (__float_as_uint(c + 8388608.0f) & 0xFu) << (4 * (i & 7));
+        }
       }
     }
     if (row_ok) {
