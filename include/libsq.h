@@ -65,9 +65,8 @@ enum {
 };
 enum { SQ_F16 = 0, SQ_BF16 = 1 };
 /* GEMM paths: AUTO picks by M (sq_w4a16_gemm); DECODE = the mma.sync kernel (M <= 16),
- * PREFILL = the tcgen05 kernel with Ŵ in TMEM (any M), DECODE_TC = the tcgen05 kernel with
- * exact (q - Z) operands and per-group accumulators (M <= 64). */
-enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2, SQ_PATH_DECODE_TC = 3 };
+ * PREFILL = the tcgen05 kernel with Ŵ in TMEM (any M). */
+enum { SQ_PATH_AUTO = 0, SQ_PATH_DECODE = 1, SQ_PATH_PREFILL = 2 };
 /* Process-wide launch options (sq_set_option):
  *  SQ_OPT_PDL (default 1): launch the GEMM kernels with programmatic dependent
  *    launch, so a kernel's prologue overlaps the previous kernel's tail; every

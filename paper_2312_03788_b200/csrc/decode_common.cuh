@@ -1,4 +1,4 @@
-// Shared pieces of the decode kernels (k_decode.cu: mma.sync; k_dtc.cu: tcgen05): the exact
+// Shared pieces of the decode kernel (k_decode.cu) and its variants: the exact
 // int4 -> (q - Z) conversion and the persistent stream-K / row-block work split.
 #pragma once
 

@@ -49,11 +49,8 @@ int num_sms() {
 }
 
 constexpr int kDecodeMaxM = 16;
-constexpr int kDecodeTcMaxM = 64;
 
-size_t ws_partials_bytes() {
-  return std::max({decode_partials_bytes(), prefill_partials_bytes(), dtc_partials_bytes()});
-}
+size_t ws_partials_bytes() { return std::max(decode_partials_bytes(), prefill_partials_bytes()); }
 
 static int g_opt_pdl = 1;
 static int g_opt_decode_schedule = SQ_SCHED_AUTO;
@@ -188,7 +185,7 @@ size_t sq_w4a16_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int group)
   (void)group;
   if (N <= 0 || K <= 0 || M < 0) return 0;
   // enough for either path, so one buffer serves SQ_PATH_AUTO and the explicit paths
-  return std::max({decode_workspace_bytes(N), dtc_workspace_bytes(N), prefill_workspace_bytes(M, N, K)});
+  return std::max(decode_workspace_bytes(N), prefill_workspace_bytes(M, N, K));
 }
 
 sq_status sq_workspace_reset(void* workspace, size_t workspace_bytes, void* stream) {
@@ -225,17 +222,6 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
                                   st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
     return cuda_status(e, "decode");
-  }
-  if (path == SQ_PATH_DECODE_TC) {
-    if (M > kDecodeTcMaxM || group != 128)
-      return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: tcgen05 decode path needs M <= %d and group 128", kDecodeTcMaxM);
-    const size_t need = dtc_workspace_bytes(N);
-    if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
-      return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: tcgen05 decode needs %zu workspace bytes (16-byte aligned)", need);
-    const char* why = nullptr;
-    cudaError_t e = launch_dtc(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, workspace, wstatic, st, &why);
-    if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm tcgen05 decode: %s", why);
-    return cuda_status(e, "decode_tc");
   }
   if (path == SQ_PATH_PREFILL) {
     const size_t need = prefill_workspace_bytes(M, N, K);

@@ -49,12 +49,6 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
                           const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws,
                           bool weights_static, cudaStream_t st, const char** why, const ArParams* ar = nullptr);
 
-// tcgen05 decode for 9 <= M <= 64 (k_dtc.cu)
-size_t dtc_partials_bytes();
-size_t dtc_workspace_bytes(int64_t N);
-cudaError_t launch_dtc(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                       void* Y, int M, int N, int K, void* ws, bool weights_static, cudaStream_t st, const char** why);
-
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
                            const uint16_t* zeros, void* Y, int M, int N, int K, int group,

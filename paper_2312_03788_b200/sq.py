@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libsq.so")
 
 SQ_OK, SQ_ERR_NULL, SQ_ERR_SHAPE, SQ_ERR_UNSUPPORTED, SQ_ERR_ALIGN, SQ_ERR_CUDA, SQ_ERR_WORKSPACE = range(7)
 SQ_F16, SQ_BF16 = 0, 1
-SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL, SQ_PATH_DECODE_TC = 0, 1, 2, 3
+SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
 SQ_OPT_PDL, SQ_OPT_DECODE_SCHEDULE, SQ_OPT_DECODE_GRID_LIMIT = 1, 3, 5
 SQ_GEMM_WEIGHTS_STATIC = 1
 SQ_SCHED_AUTO, SQ_SCHED_STREAMK, SQ_SCHED_ROWBLOCK = 0, 1, 2

@@ -370,24 +370,6 @@ def test_gemm_edge_groups(path, M, dtype):
     assert ratio <= 1.0, ratio
 
 
-@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("M", [1, 9, 16, 17, 24, 32, 33, 48, 64])
-@pytest.mark.parametrize("N,K", [(264, 1152), (1024, 2048), (2048, 4096)])
-def test_gemm_decode_tc_parity(M, N, K, dtype):
-    """The tcgen05 decode kernel (SQ_PATH_DECODE_TC, M <= 64): a ragged 128-row block
-    (N = 264), a ragged 4-group unit (K = 1152 = 9 groups), stream-K fixups (2048 x 4096 on
-    148 CTAs), every token-tile size (16, 32, 64) and ragged token counts, against the
-    oracle element by element; repeated launches are bit-identical."""
-    c = _gemm_case(M, N, K, dtype, sq.SQ_PATH_DECODE_TC, seed=M + N)
-    c.check(dtype)
-    if N == 2048:
-        x = torch.randn(M, K, device=DEV).to(dtype)
-        q = sq.quantize_pack_groupwise(torch.randn(N, K, device=DEV).half() * 0.02)
-        ys = [sq.w4a16_gemm(x, q, path=sq.SQ_PATH_DECODE_TC) for _ in range(3)]
-        torch.cuda.synchronize()
-        assert all(torch.equal(ys[0], yy) for yy in ys[1:])
-
-
 # ------------------------------------------------------------------ N3: group sizes 64 / 32
 @pytest.mark.parametrize("group", [32, 64])
 @pytest.mark.parametrize("N,K", [(264, 384), (512, 1024)])
