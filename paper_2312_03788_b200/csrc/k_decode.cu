@@ -151,16 +151,6 @@ __device__ __forceinline__ void tma_3d_hint(uint32_t dst, const CUtensorMap* m, 
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy) : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* m, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1)
-               : "memory");
-}
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n"
@@ -322,16 +312,6 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
           mbar_expect_tx(fb, C::TX);
           load_weights(sbase + pre * C::STAGE, fb, sc.u);
         }
-#ifdef SQ_DEC_L2PF
-        // the units after the ring: HBM -> L2 while this kernel waits for its predecessor
-        // (and while the predecessor's tail runs), so the startup bubble streams weights
-        for (int k = 0; k < SQ_DEC_L2PF && sc.valid(); ++k, sc.next(wk)) {
-          const int rb = sc.u / wk.upb, g0 = (sc.u % wk.upb) * GPS;
-          tma_prefetch_l2_3d(&tm_w, 0, rb * BN, g0);
-          tma_prefetch_l2_2d(&tm_s, rb * BN, g0);
-          tma_prefetch_l2_2d(&tm_z, rb * BN, g0);
-        }
-#endif
       }
       pdl_wait();  // X (and everything after) may be the previous kernel's output
       int s = 0;
@@ -913,14 +893,6 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
     return launch_small_group<64>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
   if (group == 32)
     return launch_small_group<32>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
-#ifdef SQ_DEC_M1_SLOT3
-  // experiment: M = 1 with the 74-KB three-CTA configuration but only two CTAs per SM, so
-  // the next kernel's first CTAs can become resident (and stream their weights) in the
-  // third slot while this kernel's tail runs
-  if (M == 1 && ar.world == 0)
-    return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why, 2)
-                : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why, 2);
-#endif
   if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
     // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
     // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
