@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--ar", choices=["peer", "nccl"], default="peer",
                     help="row-parallel all-reduce at N > 1: one-shot over peer memory, or NCCL")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-gates", action="store_true", help="skip the per-shape gate chains (ncu launch lists)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--backend", default="nccl", help="collective backend (gloo: test the TP path "
@@ -550,7 +551,7 @@ def main():
     # ---------------- BASELINE.json configs[3] decode batches above M_dec (32, 64): the
     # same stack pass at those M (the prefill kernel serves them), reported next to per_m
     c4 = {}
-    for M in [int(x) for x in a.c4_m.split(",") if x]:
+    for M in ([] if a.skip_gates else [int(x) for x in a.c4_m.split(",") if x]):
         b4 = stack.make_buffers(st, M, dev)
         ws4 = torch.zeros(max(16, max(sq.w4a16_gemm_workspace_bytes(M, sh.N, sh.K) for sh in st.shards)),
                           dtype=torch.uint8, device=dev)
@@ -577,7 +578,7 @@ def main():
     # its 48 layers (48 dependent launches of one shape, the stack's own resident weights,
     # 48 x the shape's bytes >> L2) in one CUDA graph; decode at every M of the step
     gates = {"decode": {}, "prefill": {}}
-    if world == 1:
+    if world == 1 and not a.skip_gates:
         for si, sh in enumerate(st.shards):
             rows = {}
             for b in bufs:
@@ -712,7 +713,7 @@ def main():
                                 "kernel": "sq::prefill_kernel (TMA + tcgen05.mma, A in TMEM)",
                                 "peak_source": f"{peaks_src} bf16_tflops (fp16 dense = bf16 dense)",
                                 "flops_per_launch": flops_rank / n_l}}
-        if world == 1:  # §8(d) prefill gate per 34B shape (each over the pass's layers)
+        if world == 1 and not a.skip_gates:  # §8(d) prefill gate per 34B shape (each over the pass's layers)
             for si, sh in enumerate(pst.shards):
                 def pchain(si=si, sh=sh):
                     for row in pst.layers:
@@ -775,7 +776,7 @@ def main():
                  "what": "sq_smooth_scales (w_max + Eq. 6) + sq_quantize_pack_groupwise for one layer"}
         del Ws
 
-    # ---------------- N2: single-layer α grid search (calibration, PAPER.md:164, :213)
+    # ---------------- N2: single-layer α grid search (calibration, PAPER.md:166, :213)
     calib_res = None
     if not a.skip_calib and rank == 0:
         from paper_2312_03788_b200 import calib

@@ -215,7 +215,7 @@ SQ_API sq_status sq_w4a16_gemm_path(const void* X, int x_dtype,
 
 /*
  * ---- Calibration: single-layer smoothing-strength search ----
- * The grid search over alpha in {0, 0.05, ..., 1} (PAPER.md:164, :213) that minimizes
+ * The grid search over alpha in {0, 0.05, ..., 1} (PAPER.md:166, :213) that minimizes
  * the Eq. 4 loss  E(alpha) = || X W^T - Xhat_alpha What_alpha^T ||^2  of one layer
  * is host logic (paper_2312_03788_b200/calib.py) over the calls above
  * plus these two device steps.

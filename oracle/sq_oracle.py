@@ -352,7 +352,7 @@ def fold_rows(W: np.ndarray, d: np.ndarray, w_dtype: str = "f16") -> np.ndarray:
 
 
 def alpha_grid() -> np.ndarray:
-    """The smoothing strengths searched: 0 to 1 at an interval of 0.05 (PAPER.md:164
+    """The smoothing strengths searched: 0 to 1 at an interval of 0.05 (PAPER.md:166
     "grid search with an interval of 0.05 between 0 and 1"), 21 values,
     each the double nearest to i/20."""
     return np.array([i / 20.0 for i in range(21)], dtype=np.float64)
@@ -377,9 +377,9 @@ def layer_loss(X: np.ndarray, W: np.ndarray, alpha: float, group: int = 128,
 
 def alpha_search(X: np.ndarray, W: np.ndarray, group: int = 128, x_dtype: str = "f16",
                  alphas=None):
-    """Grid search of the smoothing strength (PAPER.md:164, :213) for ONE layer: the α of
+    """Grid search of the smoothing strength (PAPER.md:166, :213) for ONE layer: the α of
     the grid with the smallest Eq. 4 loss; ties go to the smallest α (the first minimum
-    in grid order).  The paper minimizes the loss of the entire model (PAPER.md:164);
+    in grid order).  The paper minimizes the loss of the entire model (PAPER.md:166);
     the per-layer objective is this repo's reading.
     Returns (best_alpha, losses fp64[len(alphas)])."""
     alphas = alpha_grid() if alphas is None else np.asarray(alphas, dtype=np.float64)

@@ -1,6 +1,6 @@
 """Single-layer smoothing-strength search on the GPU.
 
-PAPER.md:164 / :213: "We use grid search with an interval of 0.05 between 0 and 1 to
+PAPER.md:166 / :213: "We use grid search with an interval of 0.05 between 0 and 1 to
 search for the smoothing strength that minimizes the quantization loss", with the loss of
 Eq. 4.  Per α of the grid (21 values):
 
@@ -25,7 +25,7 @@ import torch
 
 from . import sq
 
-#: the searched smoothing strengths (PAPER.md:164): i / 20 for i = 0..20
+#: the searched smoothing strengths (PAPER.md:166): i / 20 for i = 0..20
 ALPHA_GRID = tuple(i / 20.0 for i in range(21))
 
 

@@ -373,7 +373,7 @@ def test_p14_tp_shards():
 
 # ---------------------------------------------------------------- N2: α grid search
 def test_n2_alpha_grid():
-    """PAPER.md:164 / :213: grid over [0, 1] at an interval of 0.05 -> 21 points."""
+    """PAPER.md:166 / :213: grid over [0, 1] at an interval of 0.05 -> 21 points."""
     g = oracle.alpha_grid()
     assert len(g) == 21 and g[0] == 0.0 and g[-1] == 1.0
     assert np.allclose(np.diff(g), 0.05, atol=1e-15, rtol=0)

@@ -1,6 +1,6 @@
 """Turn gpurun_out/ ncu captures + the bench line into committed summaries under profiles/.
 
-python tools/make_profiles.py <round-tag>
+python tools/make_profiles.py <round-tag> [capture-dir]   (default capture dir: gpurun_out/<round-tag>)
 """
 import collections
 import csv
@@ -73,19 +73,39 @@ def launches(path):
     return tot, cnt
 
 
+def launch_summary(src, dst):
+    tot, cnt = launches(src)
+    T = sum(tot.values())
+    with open(dst, "w") as fh:
+        fh.write("ncu --metrics gpu__time_duration.sum --clock-control none of `python bench.py --steps 1 "
+                 "--warmup 3 --skip-prefill --skip-quant --skip-calib --skip-7b --skip-e2e --skip-cpu "
+                 "--skip-gates` (the headline decode step: 48 layers x 4 linears x M in {1,4,16}, plus "
+                 "setup/quantize and per-M passes; cold-cache, serialised launches: compare shares, not "
+                 "absolutes)\n")
+        for k, v in sorted(tot.items(), key=lambda t: -t[1]):
+            fh.write(f"{k[:80]:80s} n={cnt[k]:5d} total_us={v / 1e3:10.1f} share={100 * v / T:5.1f}% "
+                     f"avg_us={v / cnt[k] / 1e3:8.2f}\n")
+
+
 def main():
     tag = sys.argv[1]
+    if tag == "launches-only":  # <csv> <out.txt>: summarise an ncu launch list where it was taken
+        launch_summary(sys.argv[2], sys.argv[3])
+        return
+    global OUT
+    OUT = sys.argv[2] if len(sys.argv) > 2 else os.path.join(OUT, tag)
     def gemm_b(M, K, N):
         return K * N // 2 + 4 * N * (K // 128) + 2 * M * K + 2 * M * N
-    caps = [("decode", "prof_decode_m1.ncu-rep", "decode GEMM, M=1, K=8192, N=44032 (34B gate|up)",
+    caps = [("decode", "prof_decode_m1_gateup.ncu-rep", "decode GEMM, M=1, K=8192, N=44032 (34B gate|up)",
              gemm_b(1, 8192, 44032)),
-            ("decode_m16", "prof_decode_m16.ncu-rep", "decode GEMM, M=16, K=8192, N=44032",
+            ("decode_m16", "prof_decode_m16_gateup.ncu-rep", "decode GEMM, M=16, K=8192, N=44032",
              gemm_b(16, 8192, 44032)),
-            ("prefill", "prof_prefill.ncu-rep", "prefill GEMM, M=2048, K=8192, N=22016",
+            ("decode_m1_oproj", "prof_decode_m1_oproj.ncu-rep", "decode GEMM, M=1, K=8192, N=8192 (34B o_proj)",
+             gemm_b(1, 8192, 8192)),
+            ("prefill", "prof_prefill_gate.ncu-rep", "prefill GEMM, M=2048, K=8192, N=22016",
              gemm_b(2048, 8192, 22016)),
             ("quantize", "prof_quant.ncu-rep", "quantize/pack, N=22016, K=8192, with s",
-             2 * 22016 * 8192 + 4 * 8192 + 22016 * 8192 // 2 + 4 * 22016 * 64),
-            ("smooth", "prof_smooth.ncu-rep", "weight column abs-max, N=22016, K=8192", 2 * 22016 * 8192)]
+             2 * 22016 * 8192 + 4 * 8192 + 22016 * 8192 // 2 + 4 * 22016 * 64)]
     summ = {"round": tag, "how": "ncu --set full --clock-control none --import-source on (cold cache, "
                                    "one launch after warm-up) via tools/ncu_target.py"}
     for key, f, what, alg in caps:
@@ -103,9 +123,11 @@ def main():
         tot, cnt = launches(lp)
         T = sum(tot.values())
         with open(os.path.join(PROF, f"launches_{tag}.txt"), "w") as fh:
-            fh.write("ncu --metrics gpu__time_duration.sum --clock-control none of `python bench.py --steps 2 "
-                     "--warmup 1 --layers 2 --prefill-layers 1 --skip-e2e --skip-cpu --no-graph` "
-                     "(cold-cache, serialised launches: compare shares, not absolutes; includes setup kernels)\n")
+            fh.write("ncu --metrics gpu__time_duration.sum --clock-control none of `python bench.py --steps 1 "
+                     "--warmup 3 --skip-prefill --skip-quant --skip-calib --skip-7b --skip-e2e --skip-cpu "
+                     "--skip-gates` (the headline decode step: 48 layers x 4 linears x M in {1,4,16}, plus "
+                     "setup/quantize and per-M passes; cold-cache, serialised launches: compare shares, not "
+                     "absolutes)\n")
             for k, v in sorted(tot.items(), key=lambda t: -t[1]):
                 fh.write(f"{k[:80]:80s} n={cnt[k]:5d} total_us={v / 1e3:10.1f} share={100 * v / T:5.1f}% "
                          f"avg_us={v / cnt[k] / 1e3:8.2f}\n")
