@@ -32,39 +32,54 @@ namespace sq {
 namespace {
 
 constexpr int BM = 128;        // weight rows per tile (MMA M, TMEM lanes)
-constexpr int BT = 256;        // tokens per tile (MMA N max)
-constexpr int BK = 64;         // k per X stage / A stage
-constexpr int kGroup = 128;
-constexpr int NSX = 4;         // X stages (SMEM)
-constexpr int NSC = 8;         // code+scale stages (SMEM), one group each
-constexpr int NSA = 4;         // dequantized-A stages (TMEM, 32 columns each; D + A <= 512)
-constexpr int kDQW = 8;        // dequant/epilogue warps: two per TMEM lane quarter
+constexpr int kGroup = 128;    // k per code stage (one quantization-group column), A stage and X stage
+constexpr int kBTMax = 256;    // tokens per tile, widest configuration (MMA N max)
 constexpr int kDequantWarp0 = 4;
-constexpr int kThreads = (kDequantWarp0 + kDQW) * 32;
-constexpr int kColSplit = kDQW / 4;  // warps sharing a lane quarter split the work / token columns
-// 8 dequant warps: the two warps of a lane quarter take alternate 64-k stages (k-halves of
-// each group) instead of the two 32-k halves of every stage, so two A stages are in flight
-// at once and the tcgen05.st -> wait::st -> arrive latency of one overlaps the other's math
-constexpr bool kStageSplit = kColSplit == 2;
-constexpr int kAFullCount = kStageSplit ? kDQW / 2 : kDQW;
+constexpr int C_STAGE_BYTES = BM * kGroup / 2;  // packed codes of a stage, 64 B per row
+constexpr int SZ_BYTES = (kGroup / 32) * BM * 2;  // Δ (or Z) rows of a stage: [128 / GS][BM] fp16, GS >= 32
 
-constexpr int X_STAGE_BYTES = BT * BK * 2;        // 32 KB
-constexpr int C_STAGE_BYTES = BM * (kGroup / 2);  // 8 KB
-constexpr int SZ_BYTES = 4 * BM * 2;              // Δ (or Z) rows of one 128-k stage: [128 / GS][BM] fp16, GS >= 32
-
-constexpr int OFF_X = 0;
-constexpr int OFF_C = OFF_X + NSX * X_STAGE_BYTES;
-constexpr int OFF_S = OFF_C + NSC * C_STAGE_BYTES;
-constexpr int OFF_Z = OFF_S + NSC * SZ_BYTES;
-constexpr int OFF_BAR = OFF_Z + NSC * SZ_BYTES;
-constexpr int NUM_BARS = 2 * NSX + 2 * NSC + 2 * NSA + 2;
-constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
-constexpr int SMEM_BYTES = OFF_TMEM + 16;
-constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;  // slack for 1024 B alignment
-
-constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t D_COL = 0;      // accumulator: columns [0, 256)
-constexpr uint32_t A_COL = 256;    // A stages: columns [256, 256 + 32*NSA)
+// Tile configuration by token-tile width BT.  A 128-k code stage (packed
+// codes + Δ/Z rows, one TMA box each) holds 128 / KA "A stages" of KA k; each A stage is
+// converted into KA / 2 TMEM columns by one set of four dequant warps (one per TMEM lane
+// quarter) and consumed with KA / 16 MMAs against an X stage of KA k.  The R warp sets take
+// the A stages of the CTA's sequence round robin (i = r, r + R, ...), so R stages are in
+// conversion at once and one set's barrier hand-offs overlap the others' arithmetic.  The
+// accumulator takes BT TMEM columns, the A ring the rest.
+//  * BT = 256 (large M, tensor-bound): KA = 64, R = 2 -- the two sets split every code stage.
+//  * BT = 64 / 128 (one token tile, M <= 128: weight streaming, bound by the dequant warps):
+//    KA = 128, R = 3 (16 warps, 128 registers/thread).  With two sets each warp spent
+//    ~850-1050 cycles converting a stage and ~650 more in barrier checks and hand-offs
+//    (profiles/r02/prefill_midm_trace.txt); whole-group stages halve the hand-offs per weight
+//    and the third set fills the sub-partition while another waits.
+template <int kBT>
+struct PCfg {
+  static constexpr int BT = kBT;
+  static constexpr int KA = kBT == kBTMax ? 64 : 128;  // k per A stage and per X stage
+  static constexpr int APS = kGroup / KA;               // A stages per code stage
+  static constexpr int R = kBT == kBTMax ? 2 : 3;       // dequant warp sets
+  static constexpr int DQW = 4 * R;                     // dequant / epilogue warps
+  static constexpr int THREADS = (kDequantWarp0 + DQW) * 32;
+  static constexpr int X_SUB_BYTES = BT * 128;          // one 64-k SWIZZLE_128B box of BT rows
+  static constexpr int X_STAGE_BYTES = (KA / 64) * X_SUB_BYTES;
+  static constexpr int NSX = kBT == kBTMax ? 4 : kBT == 128 ? 3 : 6;    // X stages (SMEM)
+  static constexpr int NSC = kBT == kBTMax ? 8 : kBT == 128 ? 10 : 12;  // code stages (SMEM)
+  static constexpr int NSA = kBT == kBTMax ? 4 : (512 - kBT) / (KA / 2);  // A stages (TMEM)
+  static_assert(APS == 1 || APS == R, "each set takes one A stage of every code stage, or whole code stages");
+  static constexpr int OFF_X = 0;
+  static constexpr int OFF_C = OFF_X + NSX * X_STAGE_BYTES;
+  static constexpr int OFF_S = OFF_C + NSC * C_STAGE_BYTES;
+  static constexpr int OFF_Z = OFF_S + NSC * SZ_BYTES;
+  static constexpr int OFF_BAR = OFF_Z + NSC * SZ_BYTES;
+  static constexpr int NUM_BARS = 2 * NSX + 2 * NSC + 2 * NSA + 2;
+  static constexpr int OFF_TMEM = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16;
+  static constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;  // slack for 1024 B alignment
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t D_COL = 0;   // accumulator: columns [0, BT)
+  static constexpr uint32_t A_COL = BT;  // A stages: columns [BT, BT + NSA * KA / 2)
+  static_assert(A_COL + NSA * (KA / 2) <= TMEM_COLS, "TMEM budget");
+  static_assert(SMEM_ALLOC <= 227 * 1024, "SMEM budget");
+};
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -112,28 +127,50 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
-// The MMA issuer is a whole warp in warp-uniform control flow and the tcgen05 instruction is
-// predicated on elect.sync: the descriptors then live in uniform registers and one MMA
+// The MMA issuer is a whole warp in warp-uniform control flow and the tcgen05 instructions
+// are predicated on elect.sync: the descriptors then live in uniform registers and one MMA
 // issues every few cycles.  Issued from a divergent single-lane branch instead, every MMA
-// pays a per-instruction uniform-register round trip (measured ~160-220 cycles per MMA,
-// tools/micro/mma_rate.cu, vs the 128-cycle tensor floor of a 128x256x16 MMA).
+// pays a per-instruction uniform-register round trip (~160-220 cycles per MMA,
+// profiles/r02/tcgen05_mma_issue_rate.txt, vs the 128-cycle tensor floor of a 128x256x16 MMA).
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                          uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e, p;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
-      : "memory");
+// One A stage's worth of MMAs (KA / 16 of them, K = 16 each) under a single elect.sync: the
+// A address steps 8 TMEM columns and the B descriptor 32 bytes (2 in its >> 4 address field)
+// per MMA, with a jump to the second 64-k X box after four.  One asm block keeps the issue
+// stream at a few uniform-datapath instructions per MMA -- the MMA warp shares its SM
+// sub-partition with two dequant warps, so every instruction it issues costs about three
+// cycles (profiles/r02/prefill_midm_trace.txt).
+template <int NMMA>
+__device__ __forceinline__ void tc_mma_ts_stage(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc0, uint64_t b_desc1,
+                                                uint32_t idesc, uint32_t accum) {
+  static_assert(NMMA == 4 || NMMA == 8, "64 or 128 k per A stage");
+#define SQ_MMA_I(A, B, P) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [" A "], " B ", %4, " P ";\n"
+#define SQ_MMA_NEXT "add.u32 a, a, 8;\nadd.u64 b, b, 2;\n"
+  if constexpr (NMMA == 4) {
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b32 a;\n.reg .b64 b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 0, 0;\n"
+        "mov.b32 a, %1;\nmov.b64 b, %2;\n" SQ_MMA_I("a", "b", "p") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t")
+        SQ_MMA_NEXT SQ_MMA_I("a", "b", "t") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t") "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc0), "l"(b_desc1), "r"(idesc), "r"(accum)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b32 a;\n.reg .b64 b;\n"
+        "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %5, 0;\nsetp.eq.b32 t, 0, 0;\n"
+        "mov.b32 a, %1;\nmov.b64 b, %2;\n" SQ_MMA_I("a", "b", "p") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t")
+        SQ_MMA_NEXT SQ_MMA_I("a", "b", "t") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t")
+        "add.u32 a, a, 8;\nmov.b64 b, %3;\n" SQ_MMA_I("a", "b", "t") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t")
+        SQ_MMA_NEXT SQ_MMA_I("a", "b", "t") SQ_MMA_NEXT SQ_MMA_I("a", "b", "t") "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc0), "l"(b_desc1), "r"(idesc), "r"(accum)
+        : "memory");
+  }
+#undef SQ_MMA_I
+#undef SQ_MMA_NEXT
 }
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
@@ -170,6 +207,19 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)
 }
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// shared-window loads: the 1024-aligned dynamic-smem pointer is generic to the compiler, and
+// generic loads of the code stage would take the long-scoreboard path
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
+  return v;
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups
@@ -279,17 +329,21 @@ struct PSched {
   }
 };
 
-template <bool kBF16, int GS>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kBF16, int GS, int kBT>
+__global__ void __launch_bounds__(PCfg<kBT>::THREADS, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
                uint16_t* __restrict__ Y, int M, int N, int K, int early_weights, int x_bytes,
                int sk, int cta_q, int cta_r, float* __restrict__ partials, int* __restrict__ counters) {
+  using C = PCfg<kBT>;
+  constexpr int BT = C::BT, KA = C::KA, APS = C::APS, R = C::R, DQW = C::DQW;
+  constexpr int NSX = C::NSX, NSC = C::NSC, NSA = C::NSA;
+  constexpr int SUBS = kGroup / GS;  // Δ/Z rows per stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = sbase + OFF_BAR;
+  const uint32_t bar0 = sbase + C::OFF_BAR;
   auto x_full = [&](int i) { return bar0 + 8u * i; };
   auto x_empty = [&](int i) { return bar0 + 8u * (NSX + i); };
   auto c_full = [&](int i) { return bar0 + 8u * (2 * NSX + i); };
@@ -298,21 +352,20 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   auto a_empty = [&](int i) { return bar0 + 8u * (2 * NSX + 2 * NSC + NSA + i); };
   const uint32_t d_full = bar0 + 8u * (2 * NSX + 2 * NSC + 2 * NSA);
   const uint32_t d_empty = d_full + 8u;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEM);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n_tiles = (N + BM - 1) / BM;
   const int m_tiles = (M + BT - 1) / BT;
   const int num_tiles = n_tiles * m_tiles;
-  const int num_kb = K / BK;
-  const int G = K / kGroup;
+  const int G = K / kGroup;  // stages per tile (the schedule's unit)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSX; ++i) { mbar_init(x_full(i), 1); mbar_init(x_empty(i), 1); }
-    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), kDQW); }
-    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), kAFullCount); mbar_init(a_empty(i), 1); }
+    for (int i = 0; i < NSC; ++i) { mbar_init(c_full(i), 1); mbar_init(c_empty(i), 4 * APS); }
+    for (int i = 0; i < NSA; ++i) { mbar_init(a_full(i), 4); mbar_init(a_empty(i), 1); }
     mbar_init(d_full, 1);
-    mbar_init(d_empty, kDQW);
+    mbar_init(d_empty, DQW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
@@ -325,7 +378,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
@@ -335,7 +388,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   pdl_launch_dependents();
 
   if (warp == 0) {
-    // ===================== TMA producer: activations =====================
+    // ===================== TMA producer: activations, one X stage per A stage =====================
     if (lane == 0) {
       pdl_wait();  // X may be the previous kernel's output
       int xs = 0;
@@ -343,10 +396,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
         const int tile = sc.tile;
         const int m0 = (tile % m_tiles) * BT;
-        for (int kb = 2 * sc.g0; kb < 2 * sc.g1; ++kb) {
+        for (int kb = APS * sc.g0; kb < APS * sc.g1; ++kb) {
           mbar_wait(x_empty(xs), xph ^ 1);
           mbar_expect_tx(x_full(xs), x_bytes);
-          tma_load_2d(sbase + OFF_X + xs * X_STAGE_BYTES, &tm_x, x_full(xs), kb * BK, m0);
+#pragma unroll
+          for (int h = 0; h < KA / 64; ++h)
+            tma_load_2d(sbase + C::OFF_X + xs * C::X_STAGE_BYTES + h * C::X_SUB_BYTES, &tm_x, x_full(xs),
+                        kb * KA + h * 64, m0);
           if (++xs == NSX) { xs = 0; xph ^= 1; }
         }
       }
@@ -362,11 +418,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const int n0 = (tile / m_tiles) * BM;
         for (int g = sc.g0; g < sc.g1; ++g) {
           mbar_wait(c_empty(cs), cph ^ 1);
-          constexpr int SUB = kGroup / GS;  // quantization groups per 128-k stage
-          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SUB * BM * 2);
-          tma_load_2d(sbase + OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
-          tma_load_2d(sbase + OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g * SUB);
-          tma_load_2d(sbase + OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g * SUB);
+          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SUBS * BM * 2);
+          tma_load_2d(sbase + C::OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
+          tma_load_2d(sbase + C::OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g * SUBS);
+          tma_load_2d(sbase + C::OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g * SUBS);
           if (++cs == NSC) { cs = 0; cph ^= 1; }
         }
       }
@@ -384,18 +439,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         mbar_wait(d_empty, dph ^ 1);  // epilogue has drained the accumulator
         dph ^= 1;
         tc_fence_after();
-        const int kb0 = 2 * sc.g0;
-        for (int kb = kb0; kb < 2 * sc.g1; ++kb) {
+        for (int kb = APS * sc.g0; kb < APS * sc.g1; ++kb) {
           mbar_wait(a_full(as), aph);
           mbar_wait(x_full(xs), xph);
           tc_fence_after();
-          const uint32_t xaddr = sbase + OFF_X + xs * X_STAGE_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t a_tmem = tmem_base + A_COL + (uint32_t)as * (BK / 2) + (uint32_t)kk * 8;
-            const uint64_t bdesc = make_sw128_desc(xaddr + kk * 32);
-            tc_mma_ts(tmem_base + D_COL, a_tmem, bdesc, idesc, (kb != kb0 || kk) ? 1u : 0u);
-          }
+          const uint32_t xaddr = sbase + C::OFF_X + xs * C::X_STAGE_BYTES;
+          tc_mma_ts_stage<KA / 16>(tmem_base + C::D_COL, tmem_base + C::A_COL + (uint32_t)as * (KA / 2),
+                                   make_sw128_desc(xaddr), make_sw128_desc(xaddr + C::X_SUB_BYTES), idesc,
+                                   kb != APS * sc.g0 ? 1u : 0u);
           tc_commit(x_empty(xs));
           tc_commit(a_empty(as));
           if (++xs == NSX) { xs = 0; xph ^= 1; }
@@ -407,69 +458,80 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   } else if (warp >= kDequantWarp0) {
     // ===================== dequant + epilogue (thread = weight row = TMEM lane) =====
     const int q = (warp - kDequantWarp0) % 4;   // TMEM sub-partition (warp % 4)
-    const int ch = (warp - kDequantWarp0) / 4;  // column split among warps of one quarter
+    const int ch = (warp - kDequantWarp0) / 4;  // warp set: stages j = ch (mod R) of the CTA's sequence
     const int row = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    int cs = 0;
-    uint32_t cph = 0, dph = 0;
-    int ai = 0;  // A-ring stage counter
+    const int sw = (row >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk c of the row sits at c ^ ((row >> 1) & 3)
+    uint32_t dph = 0;
+    int j = 0;  // code-stage counter over the CTA's whole sequence (ring slot j % NSC, phase (j / NSC) & 1)
     for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
       const int tile = sc.tile;
       const int n0 = (tile / m_tiles) * BM;
       const int m0 = (tile % m_tiles) * BT;
-      for (int g = sc.g0; g < sc.g1; ++g) {
-        // the two warps of a lane quarter take alternate 64-k halves of each 128-k stage, so
-        // two A stages are in flight at once and the tcgen05.st -> wait::st -> arrive latency
-        // of one overlaps the other's math
-        static_assert(kStageSplit, "two dequant warps per TMEM lane quarter");
-        mbar_wait(c_full(cs), cph);
-        const uint8_t* crow = smem + OFF_C + cs * C_STAGE_BYTES + row * 64;
-        const int sw = (row >> 1) & 3;  // SWIZZLE_64B: chunk c sits at c ^ ((row >> 1) & 3)
-        const uint4 c0v = *reinterpret_cast<const uint4*>(crow + (((2 * ch) ^ sw) << 4));
-        const uint4 c1v = *reinterpret_cast<const uint4*>(crow + (((2 * ch + 1) ^ sw) << 4));
-        // quantization groups of this warp's 64 k: one (GS >= 64) or two (GS = 32)
-        constexpr int NG = GS >= 64 ? 1 : 2;
+      for (int g = sc.g0; g < sc.g1; ++g, ++j) {
+        // this set's A stage of the code stage: t = ch (APS = R), or the whole stage (APS = 1)
+        if (APS == 1 && j % R != ch) continue;
+        const int t = APS == 1 ? 0 : ch;
+        const int i = j * APS + t;  // A-stage counter
+        const int cs = j % NSC;
+        mbar_wait(c_full(cs), (j / NSC) & 1);
+        const uint32_t crow = sbase + C::OFF_C + cs * C_STAGE_BYTES + row * (kGroup / 2);
+        constexpr int NCH = KA / 32;  // 16-byte chunks of the A stage in the row
+        uint32_t words[KA / 8];
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) {
+          const uint4 v = lds128(crow + (((t * NCH + u) ^ sw) << 4));
+          words[4 * u] = v.x; words[4 * u + 1] = v.y; words[4 * u + 2] = v.z; words[4 * u + 3] = v.w;
+        }
+        constexpr int NG = KA >= GS ? KA / GS : 1;  // quantization groups in the A stage
+        constexpr int GSPAN = KA >= GS ? GS : KA;   // k of the A stage in each
         uint16_t sbits[NG], zbits[NG];
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
-          const int sub = (64 * ch + 32 * h) / GS;
-          sbits[h] = *reinterpret_cast<const uint16_t*>(smem + OFF_S + cs * SZ_BYTES + (sub * BM + row) * 2);
-          zbits[h] = *reinterpret_cast<const uint16_t*>(smem + OFF_Z + cs * SZ_BYTES + (sub * BM + row) * 2);
+          const int sub = (t * KA + h * GSPAN) / GS;
+          sbits[h] = lds16(sbase + C::OFF_S + cs * SZ_BYTES + (sub * BM + row) * 2);
+          zbits[h] = lds16(sbase + C::OFF_Z + cs * SZ_BYTES + (sub * BM + row) * 2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(c_empty(cs));
-        if (++cs == NSC) { cs = 0; cph ^= 1; }
-        const uint32_t words[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
-        uint32_t a[32];
+        uint32_t zc[NG], d2[NG];
+        float df[NG];
+        bool sat = false;  // fp16 groups with Δ > 65504 / 15 take the saturating conversion
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
           const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), __ushort_as_half(zbits[h])));
           const __half2 d2h = __half2half2(__ushort_as_half(sbits[h]));
-          const uint32_t zc = *reinterpret_cast<const uint32_t*>(&zc2);
-          const uint32_t d2 = *reinterpret_cast<const uint32_t*>(&d2h);
-          const float df = __half2float(__ushort_as_half(sbits[h]));
-          constexpr int WPG = 8 / NG;  // code words per group
-          if (!kBF16 && df > 4366.0f) {
-#pragma unroll
-            for (int wd = 0; wd < WPG; ++wd)
-              dequant8<kBF16, true>(words[h * WPG + wd], zc, d2, df, &a[4 * (h * WPG + wd)]);
-          } else {
-#pragma unroll
-            for (int wd = 0; wd < WPG; ++wd)
-              dequant8<kBF16>(words[h * WPG + wd], zc, d2, df, &a[4 * (h * WPG + wd)]);
-          }
+          zc[h] = *reinterpret_cast<const uint32_t*>(&zc2);
+          d2[h] = *reinterpret_cast<const uint32_t*>(&d2h);
+          df[h] = __half2float(__ushort_as_half(sbits[h]));
+          sat |= !kBF16 && df[h] > 4366.0f;
         }
-        // this warp's stage: k-half ch of the group -> A-ring index ai + ch
-        const int i = ai + ch;
         const int slot = i % NSA;
         mbar_wait(a_empty(slot), ((i / NSA) & 1) ^ 1);
         tc_fence_after();
-        tmem_st_32x32b_x32(tmem_base + lane_addr + A_COL + (uint32_t)slot * (BK / 2), a);
+        // dequantize and store 64 k (32 TMEM columns) at a time
+#pragma unroll
+        for (int part = 0; part < KA / 64; ++part) {
+          uint32_t a[32];
+          if (sat) {
+#pragma unroll
+            for (int wd = 0; wd < 8; ++wd) {
+              const int h = ((part * 8 + wd) * 8) / GSPAN;  // quantization group of this word
+              dequant8<kBF16, true>(words[part * 8 + wd], zc[h], d2[h], df[h], &a[4 * wd]);
+            }
+          } else {
+#pragma unroll
+            for (int wd = 0; wd < 8; ++wd) {
+              const int h = ((part * 8 + wd) * 8) / GSPAN;
+              dequant8<kBF16>(words[part * 8 + wd], zc[h], d2[h], df[h], &a[4 * wd]);
+            }
+          }
+          tmem_st_32x32b_x32(tmem_base + lane_addr + C::A_COL + (uint32_t)slot * (KA / 2) + (uint32_t)part * 32, a);
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full(slot));
-        ai += 2;
       }
       // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
       pdl_wait();  // (returns at once after the first tile) Y may be read by the previous kernel
@@ -485,9 +547,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       // stream-K partial tile: fp32 [token][row] slot of this CTA (0: first segment, 1: last)
       float* slot = partials + ((size_t)blockIdx.x * 2 + (sc.first ? 0 : 1)) * (BT * BM);
       // warps sharing a lane quarter take alternating 16-token column blocks
-      for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
+      for (int c0 = ch * 16; c0 < mt; c0 += 16 * R) {
         uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + lane_addr + D_COL + (uint32_t)c0, v);
+        tmem_ld_32x32b_x16(tmem_base + lane_addr + C::D_COL + (uint32_t)c0, v);
         tmem_ld_wait();
         if (full) {
           if (n < N) {
@@ -507,8 +569,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
       if (!full) {
         // fixup, overlapping the next segment's MMAs: the dequant warps' partial stores are
         // published by one acq_rel atomic after a barrier among them
-        int* flag = reinterpret_cast<int*>(smem + OFF_TMEM + 8);
-        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");
+        int* flag = reinterpret_cast<int*>(smem + C::OFF_TMEM + 8);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(DQW * 32) : "memory");
         const int c_lo = sc.cta_of(tile * G), c_hi = sc.cta_of(tile * G + G - 1);
         if (threadIdx.x == kDequantWarp0 * 32) {
           int prev;
@@ -516,10 +578,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
                        : "=r"(prev) : "l"(counters + tile) : "memory");
           *flag = prev == c_hi - c_lo;
         }
-        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");
+        asm volatile("bar.sync 1, %0;\n" ::"n"(DQW * 32) : "memory");
         if (*flag) {
           if (n < N) {
-            for (int c0 = ch * 16; c0 < mt; c0 += 16 * kColSplit) {
+            for (int c0 = ch * 16; c0 < mt; c0 += 16 * R) {
               float acc[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
@@ -539,7 +601,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           }
           if (threadIdx.x == kDequantWarp0 * 32) counters[tile] = 0;  // leave the workspace zeroed
         }
-        asm volatile("bar.sync 1, %0;\n" ::"n"(kDQW * 32) : "memory");  // flag reuse
+        asm volatile("bar.sync 1, %0;\n" ::"n"(DQW * 32) : "memory");  // flag reuse
       }
     }
   }
@@ -549,7 +611,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+                 "r"(C::TMEM_COLS));
   }
 }
 
@@ -585,65 +647,79 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 
 }  // namespace
 
-size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * BT * BM * sizeof(float); }
+size_t prefill_partials_bytes() { return (size_t)num_sms() * 2 * kBTMax * BM * sizeof(float); }
 
-// Stream-K over (tile x group) units when whole tiles would leave > 5 % of the last wave
-// idle at mid M (one token tile), or > 10 % on a long-K shape at large M (down_proj at
+// Token-tile width: the narrowest configuration that holds M in one tile, else 256.
+static int prefill_bt(int64_t M) { return M <= 64 ? 64 : M <= 128 ? 128 : kBTMax; }
+static int64_t prefill_tiles(int64_t M, int64_t N) {
+  const int64_t bt = prefill_bt(M);
+  return ((N + BM - 1) / BM) * ((M + bt - 1) / bt);
+}
+static int64_t prefill_stages(int64_t, int64_t K) { return K / kGroup; }  // schedule units per tile
+
+// Stream-K over (tile x code stage) units when whole tiles would leave > 5 % of the last
+// wave idle at mid M (one token tile), or > 10 % on a long-K shape at large M (down_proj at
 // M = 2048).  Elsewhere the CTAs sweeping k in lockstep share X and W tiles in L2, which
 // stream-K's staggered ranges give up (measured: o_proj/qkv at M = 2048 are faster without).
 bool prefill_streamk(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int64_t tiles = prefill_tiles(M, N);
   const int64_t P = num_sms();
   const int64_t waves = (tiles + P - 1) / P;
   const double eff = (double)tiles / (double)(waves * P);
-  if (tiles * (K / kGroup) < P) return false;
-  return M <= BT ? eff < 0.95 : (eff < 0.9 && K >= 16384);
+  if (tiles * prefill_stages(M, K) < P) return false;
+  return M <= kBTMax ? eff < 0.95 : (eff < 0.9 && K >= 16384);
 }
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (!prefill_streamk(M, N, K)) return 0;
-  const int64_t tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
-  return ws_partials_bytes() + counter_region_bytes(tiles);
+  return ws_partials_bytes() + counter_region_bytes(prefill_tiles(M, N));
 }
 
-cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws, size_t,
-                           bool weights_static, cudaStream_t st, const char** why) {
+namespace {
+template <bool kBF16, int kBT>
+auto pick_kernel(int group) {
+  return group == 32 ? prefill_kernel<kBF16, 32, kBT> : group == 64 ? prefill_kernel<kBF16, 64, kBT>
+                                                                    : prefill_kernel<kBF16, 128, kBT>;
+}
+
+template <int kBT>
+cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+                      void* Y, int M, int N, int K, int group, void* ws, bool weights_static, cudaStream_t st,
+                      const char** why) {
+  using C = PCfg<kBT>;
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
-  const int G = K / kGroup;
-  // X box: only as many token rows as the problem has (OOB rows would still cross the
-  // crossbar as zero fill)
-  const int x_rows = std::min(BT, (M + 15) / 16 * 16);
+  const int G = (int)prefill_stages(M, K);
+  // X box: 64 k (one SWIZZLE_128B row) of only as many token rows as the problem has (OOB
+  // rows would still cross the crossbar as zero fill)
+  const int x_rows = std::min(kBT, (M + 15) / 16 * 16);
   bool ok = encode_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_UINT16, X, (uint64_t)K, (uint64_t)M,
-                      (uint64_t)K * 2, BK, x_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+                      (uint64_t)K * 2, 64, x_rows, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && encode_2d(&tm_w, CU_TENSOR_MAP_DATA_TYPE_UINT8, Wq, (uint64_t)K / 2, (uint64_t)N,
                        (uint64_t)K / 2, kGroup / 2, BM, CU_TENSOR_MAP_SWIZZLE_64B);
-  const int sub = kGroup / group;  // scale / zero rows per 128-k stage
-  ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)G * sub,
-                       (uint64_t)N * 2, BM, sub, CU_TENSOR_MAP_SWIZZLE_NONE);
-  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)G * sub,
-                       (uint64_t)N * 2, BM, sub, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const int sub = kGroup / group;  // scale / zero rows per 128 k
+  const int subs = sub;
+  ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)(K / kGroup) * sub,
+                       (uint64_t)N * 2, BM, subs, CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)(K / kGroup) * sub,
+                       (uint64_t)N * 2, BM, subs, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!ok) {
     *why = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
-  const int num_tiles = ((N + BM - 1) / BM) * ((M + BT - 1) / BT);
+  const int num_tiles = (int)prefill_tiles(M, N);
   const bool sk = prefill_streamk(M, N, K);
   const int units = num_tiles * G;
   const int grid = sk ? std::min(units, num_sms()) : std::min(num_tiles, num_sms());
   const int cta_q = units / grid, cta_r = units % grid;
   float* partials = reinterpret_cast<float*>(ws);
   int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
-  auto kern = x_dtype == SQ_BF16 ? (group == 32 ? prefill_kernel<true, 32> : group == 64 ? prefill_kernel<true, 64>
-                                                                                       : prefill_kernel<true, 128>)
-                                  : (group == 32 ? prefill_kernel<false, 32> : group == 64 ? prefill_kernel<false, 64>
-                                                                                        : prefill_kernel<false, 128>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ALLOC);
+  auto kern = x_dtype == SQ_BF16 ? pick_kernel<true, kBT>(group) : pick_kernel<false, kBT>(group);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_ALLOC);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = SMEM_ALLOC;
+  cfg.blockDim = dim3(C::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_ALLOC;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -652,9 +728,23 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && weights_static;
   e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early,
-                         x_rows * BK * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
+                         x_rows * C::KA * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
+                           const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws, size_t,
+                           bool weights_static, cudaStream_t st, const char** why) {
+  switch (prefill_bt(M)) {
+    case 64:
+      return launch_bt<64>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+    case 128:
+      return launch_bt<128>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+    default:
+      return launch_bt<kBTMax>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+  }
 }
 
 }  // namespace sq

@@ -193,7 +193,7 @@ def test_gemm_decode_parity(M, N, K, dtype):
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("M", [17, 64, 256, 300, 520])
+@pytest.mark.parametrize("M", [17, 64, 65, 100, 128, 129, 256, 300, 520])
 @pytest.mark.parametrize("N,K", [(256, 512), (392, 1152), (1024, 2048)])
 def test_gemm_prefill_parity(M, N, K, dtype):
     _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M).check(dtype)

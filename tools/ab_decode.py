@@ -106,9 +106,8 @@ def main():
                     e1.record()
                     torch.cuda.synchronize()
                     times[lname].append(e0.elapsed_time(e1) * 1e3 / launches)
-            B = wb + 2 * M * K + 2 * M * N
-            if path == 2 and M >= 128:
-                B = 2 * M * N * K * PEAK_HBM / PEAK_TC  # report the fraction of the dense fp16 peak
+            # roofline time = max(bytes / HBM, flops / tensor peak), reported as HBM-equivalent bytes
+            B = max(wb + 2 * M * K + 2 * M * N, 2 * M * N * K * PEAK_HBM / (PEAK_TC * 1e3))
             row = {"shape": name, "M": M}
             for ln, ts in times.items():
                 ts = sorted(ts)[1:-1]

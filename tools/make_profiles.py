@@ -35,7 +35,11 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "hz": 1, "Khz
 
 
 def raw(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    exported = path[:-len(".ncu-rep")] + ".raw.csv"  # exported on the box (large reports stay there)
+    if os.path.exists(exported):
+        out = open(exported).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -104,13 +108,15 @@ def main():
              gemm_b(1, 8192, 8192)),
             ("prefill", "prof_prefill_gate.ncu-rep", "prefill GEMM, M=2048, K=8192, N=22016",
              gemm_b(2048, 8192, 22016)),
+            ("prefill_m32", "prof_prefill_m32_gateup.ncu-rep", "prefill GEMM, M=32, K=8192, N=44032 (mid-M)",
+             gemm_b(32, 8192, 44032)),
             ("quantize", "prof_quant.ncu-rep", "quantize/pack, N=22016, K=8192, with s",
              2 * 22016 * 8192 + 4 * 8192 + 22016 * 8192 // 2 + 4 * 22016 * 64)]
     summ = {"round": tag, "how": "ncu --set full --clock-control none --import-source on (cold cache, "
                                    "one launch after warm-up) via tools/ncu_target.py"}
     for key, f, what, alg in caps:
         p = os.path.join(OUT, f)
-        if os.path.exists(p):
+        if os.path.exists(p) or os.path.exists(p[:-len(".ncu-rep")] + ".raw.csv"):
             summ[key] = summarise(p, what)
             summ[key]["algorithmic_bytes"] = alg
             summ[key]["traffic_over_algorithmic"] = summ[key]["dram_bytes_per_launch"] / alg
@@ -119,7 +125,10 @@ def main():
     with open(os.path.join(PROF, "ncu_summary.json"), "w") as fh:
         json.dump(summ, fh, indent=1)
     lp = os.path.join(OUT, "launches.csv")
-    if os.path.exists(lp):
+    if os.path.exists(os.path.join(OUT, "launches.txt")):  # summarised on the box
+        with open(os.path.join(OUT, "launches.txt")) as src, open(os.path.join(PROF, f"launches_{tag}.txt"), "w") as fh:
+            fh.write(src.read())
+    elif os.path.exists(lp):
         tot, cnt = launches(lp)
         T = sum(tot.values())
         with open(os.path.join(PROF, f"launches_{tag}.txt"), "w") as fh:
