@@ -56,7 +56,7 @@ struct PCfg {
   static constexpr int BT = kBT;
   static constexpr int KA = kBT == kBTMax ? 64 : 128;  // k per A stage and per X stage
   static constexpr int APS = kGroup / KA;               // A stages per code stage
-  static constexpr int R = kBT == kBTMax ? 2 : 3;       // dequant warp sets
+  static constexpr int R = kBT == kBTMax ? 2 : 3;       // dequant warp sets (4 or 5: no faster)
   static constexpr int DQW = 4 * R;                     // dequant / epilogue warps
   static constexpr int THREADS = (kDequantWarp0 + DQW) * 32;
   static constexpr int X_SUB_BYTES = BT * 128;          // one 64-k SWIZZLE_128B box of BT rows

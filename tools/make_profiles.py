@@ -34,6 +34,9 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "hz": 1, "Khz
               "Ghz": 1e9}
 
 
+TAG = ""
+
+
 def raw(path):
     exported = path[:-len(".ncu-rep")] + ".raw.csv"  # exported on the box (large reports stay there)
     if os.path.exists(exported):
@@ -47,7 +50,9 @@ def raw(path):
 def summarise(path, what):
     h, units, rows = raw(path)
     r = rows[0]
-    d = {"kernel": r[h.index("Kernel Name")], "what": what, "report": os.path.basename(path)}
+    # the committed copy (profiles/<tag>/ncu/: gzipped raw page, details page, SASS source page)
+    d = {"kernel": r[h.index("Kernel Name")], "what": what,
+         "report": f"{TAG}/ncu/" + os.path.basename(path)[:-len(".ncu-rep")] + ".raw.csv.gz"}
     for k, (m, scale) in KEYS.items():
         if m not in h:
             continue
@@ -92,7 +97,8 @@ def launch_summary(src, dst):
 
 
 def main():
-    tag = sys.argv[1]
+    global TAG
+    tag = TAG = sys.argv[1]
     if tag == "launches-only":  # <csv> <out.txt>: summarise an ncu launch list where it was taken
         launch_summary(sys.argv[2], sys.argv[3])
         return
