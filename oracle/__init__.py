@@ -39,6 +39,8 @@ from .sq_oracle import (  # noqa: F401
     quantize_pack,
     pack_nibbles,
     unpack_nibbles,
+    pack_zeros_u4,
+    unpack_zeros_u4,
     dequant,
     gemm,
     quant_loss,

@@ -252,6 +252,24 @@ def unpack_nibbles(b: np.ndarray) -> np.ndarray:
     return out
 
 
+def pack_zeros_u4(zeros: np.ndarray) -> np.ndarray:
+    """Packed 4-bit zero points, the u4 variant of N3 (SURVEY.md §8(f) "a packed u4
+    zero-point variant"; SPEC.md:185-186 stores Z as u4).  Every Z is an integer 0..15
+    (Eq. 1 clamps it, reading S2), so it fits a nibble exactly.  Two per byte along the
+    output-channel axis: channel 2i in the low nibble, 2i+1 in the high nibble -- the
+    nibble order pack_nibbles uses along k.
+    zeros fp16 bits uint16[G][N] (N even) -> uint8[G][N/2]."""
+    z = np.asarray(zeros, dtype=np.uint16).view(np.float16).astype(np.float64)
+    if not np.all(np.isfinite(z)) or (z != np.round(z)).any() or (z < 0).any() or (z > 15).any():
+        raise ValueError("zero points must be integers 0..15")
+    return pack_nibbles(z.astype(np.int64))
+
+
+def unpack_zeros_u4(zeros_u4: np.ndarray) -> np.ndarray:
+    """Inverse of pack_zeros_u4: uint8[G][N/2] -> fp16 bits uint16[G][N]."""
+    return unpack_nibbles(zeros_u4).astype(np.float16).view(np.uint16)
+
+
 def quantize_pack(W: np.ndarray, s=None, group: int = 128, w_dtype: str = "f16"):
     """sq_quantize_pack_groupwise semantics: Eq. 5 fold (W' = RN(W·s)) then Eq. 1 per
     (output channel n, group of g consecutive input channels) (PAPER.md:160
@@ -292,9 +310,13 @@ def quantize_pack(W: np.ndarray, s=None, group: int = 128, w_dtype: str = "f16")
 # a6/a7: Eq. 1 line 2 dequantization and Eq. 3 linear layer
 # --------------------------------------------------------------------------
 
-def dequant(Wq: np.ndarray, scales: np.ndarray, zeros: np.ndarray, group: int = 128) -> np.ndarray:
+def dequant(Wq: np.ndarray, scales: np.ndarray, zeros: np.ndarray, group: int = 128,
+            zeros_u4: bool = False) -> np.ndarray:
     """Ŵ = (W̄ - Z)·Δ (Eq. 1 line 2), exact in fp64.
-    Wq uint8[N][K/2], scales/zeros fp16 bits [G][N] -> fp64[N][K]."""
+    Wq uint8[N][K/2], scales/zeros fp16 bits [G][N] (zeros_u4: zeros packed by
+    pack_zeros_u4, uint8[G][N/2]) -> fp64[N][K]."""
+    if zeros_u4:
+        zeros = unpack_zeros_u4(zeros)
     q = unpack_nibbles(Wq)
     N, K = q.shape
     G = K // group
@@ -306,11 +328,11 @@ def dequant(Wq: np.ndarray, scales: np.ndarray, zeros: np.ndarray, group: int = 
 
 
 def gemm(X: np.ndarray, Wq: np.ndarray, scales: np.ndarray, zeros: np.ndarray,
-         group: int = 128, x_dtype: str = "f16") -> np.ndarray:
+         group: int = 128, x_dtype: str = "f16", zeros_u4: bool = False) -> np.ndarray:
     """Eq. 3: Y = X̂·Ŵ, with Eq. 2's W_eq2 = Ŵ[N][K]^T
     (PAPER.md:95-100).  X[M][K] fp16 (or bf16 bits) -> Y fp64[M][N]."""
     x = _as_f64(X, x_dtype)
-    return x @ dequant(Wq, scales, zeros, group).T
+    return x @ dequant(Wq, scales, zeros, group, zeros_u4).T
 
 
 def quant_loss(X: np.ndarray, W: np.ndarray, W_hat: np.ndarray) -> float:
@@ -389,8 +411,8 @@ def alpha_search(X: np.ndarray, W: np.ndarray, group: int = 128, x_dtype: str = 
     return float(alphas[best]), losses
 
 
-def footprint_ratio(N: int, K: int, group: int = 128) -> float:
-    """Bytes of the W4 layout (codes + fp16 Δ + fp16 Z per group) over fp16 bytes
+def footprint_ratio(N: int, K: int, group: int = 128, zeros_u4: bool = False) -> float:
+    """Bytes of the W4 layout (codes + fp16 Δ + fp16 or u4 Z per group) over fp16 bytes
     (PAPER.md:74 "reducing the memory footprint by approximately 75%")."""
-    packed = N * K / 2 + 2 * 2 * N * (K // group)
+    packed = N * K / 2 + 2 * N * (K // group) + (0.5 if zeros_u4 else 2) * N * (K // group)
     return packed / (2.0 * N * K)

@@ -582,3 +582,44 @@ def test_n3_footprint_by_group_size():
         q = oracle.quantize_pack(synth.weights(64, 512, seed=73), None, group)
         nbytes = q["Wq"].nbytes + q["scales"].nbytes + q["zeros"].nbytes
         assert nbytes / (2.0 * 64 * 512) == want
+
+
+# ---------------------------------------------------------------- N3: packed u4 zero points
+
+def test_n3_zeros_u4_worked_example():
+    """Hand-packed example (tests/golden/zeros_u4_example.json): channel 2i in the low
+    nibble, 2i+1 in the high nibble, one byte row per group row."""
+    f = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "zeros_u4_example.json")))
+    z = np.array(f["zeros_f16_bits"], dtype=np.uint16)
+    assert z.view(np.float16).astype(float).tolist() == [[1, 2, 15, 0], [3, 3, 0, 7]]
+    assert oracle.pack_zeros_u4(z).tolist() == f["zeros_u4"]
+    assert oracle.unpack_zeros_u4(np.array(f["zeros_u4"], dtype=np.uint8)).tolist() == z.tolist()
+
+
+def test_n3_zeros_u4_roundtrip_and_same_layer():
+    """Packing loses nothing: every Z the quantizer emits (integers 0..15, incl. edge and
+    non-finite groups) survives pack/unpack bit for bit, so the dequantized layer and the
+    GEMM are identical with either zero-point layout; the u4 layout is 3/4 smaller."""
+    W = np.concatenate([synth.weights(56, 256, seed=81), synth.edge_groups(256, seed=82)[:8]])
+    W[3, 5] = np.float16(np.inf)
+    q = oracle.quantize_pack(W.astype(np.float16))
+    assert q["nonfinite"] >= 1
+    zu4 = oracle.pack_zeros_u4(q["zeros"])
+    assert zu4.shape == (q["zeros"].shape[0], q["zeros"].shape[1] // 2) and zu4.dtype == np.uint8
+    assert np.array_equal(oracle.unpack_zeros_u4(zu4), q["zeros"])
+    X = synth.activations(3, 256, seed=83).astype(np.float16)
+    ok = ~np.isnan(q["delta"]).any(axis=0)  # channels without a non-finite group
+    y16 = oracle.gemm(X, q["Wq"], q["scales"], q["zeros"])
+    y4 = oracle.gemm(X, q["Wq"], q["scales"], zu4, zeros_u4=True)
+    assert np.array_equal(y16[:, ok], y4[:, ok])
+    for group, want in ((128, 0.259765625), (32, 0.2890625)):   # (0.5 + 2.5/g) / 2
+        assert oracle.footprint_ratio(64, 512, group, zeros_u4=True) == want
+
+
+def test_n3_zeros_u4_rejects_non_codes():
+    with pytest.raises(ValueError):
+        oracle.pack_zeros_u4(np.array([[0x3C00, 0x3800]], dtype=np.uint16))   # 1, 0.5
+    with pytest.raises(ValueError):
+        oracle.pack_zeros_u4(np.array([[0x4C00, 0]], dtype=np.uint16))        # 16
+    with pytest.raises(ValueError):
+        oracle.pack_zeros_u4(np.array([[0, 0, 0]], dtype=np.uint16))          # odd N
