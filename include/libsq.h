@@ -23,13 +23,17 @@
  *    Wq[n][k/2] when k is even, the HIGH nibble when k is odd.
  *  - scales[G][N] and zeros[G][N] are fp16 bit patterns (uint16), group-major:
  *    scales[gi][n] is Delta of the group (n, k in [gi*group, (gi+1)*group)).
- *    zeros hold integers 0..15 stored as fp16.
+ *    zeros hold integers 0..15 stored as fp16.  With SQ_ZEROS_U4 (SURVEY.md §8(f) N3,
+ *    SPEC.md:185-186 "Z: u4") zeros are instead PACKED uint8[G][N/2]: Z of channel n is
+ *    the LOW nibble of byte zeros[gi][n/2] when n is even, the HIGH nibble when n is
+ *    odd (the nibble order of the codes, along n; oracle/sq_oracle.py pack_zeros_u4).
+ *    The packed layout needs N % 32 == 0 (16-byte rows for TMA), else SQ_ERR_ALIGN.
  *  - dtype codes: SQ_F16 (IEEE binary16) or SQ_BF16 (bfloat16).
  *
  * Errors:
  *  - Argument errors are detected on the host, return a status and launch
  *    nothing: NULL pointer -> SQ_ERR_NULL; negative/zero dims -> SQ_ERR_SHAPE
- *    (M == 0 is a valid no-op); group != 128, K % group != 0 or an unknown dtype
+ *    (M == 0 is a valid no-op); group not in {32, 64, 128}, K % 128 != 0 or an unknown dtype
  *    -> SQ_ERR_UNSUPPORTED; a pointer not 16-byte aligned or N % 8 != 0 ->
  *    SQ_ERR_ALIGN; a workspace that is too small -> SQ_ERR_WORKSPACE.
  *  - Launch failures return SQ_ERR_CUDA; sq_last_error() then holds the CUDA
@@ -94,6 +98,11 @@ enum { SQ_SCHED_AUTO = 0, SQ_SCHED_STREAMK = 1, SQ_SCHED_ROWBLOCK = 2 };
  *    kernel; X and every global write still wait.  Without the flag the weights are
  *    read only after the previous kernel has completed. */
 enum { SQ_GEMM_WEIGHTS_STATIC = 1u };
+/* SQ_ZEROS_U4 (GEMM and quantize flags): the zeros argument is the packed u4 layout
+ *    uint8[G][N/2] described above instead of fp16 bits uint16[G][N]; it is passed
+ *    through the same `zeros` pointer (cast).  Results are identical either way (Z is an
+ *    integer 0..15); the packed layout moves 0.5 instead of 2 bytes per group row. */
+enum { SQ_ZEROS_U4 = 2u };
 
 /* Library version (major*10000 + minor*100 + patch). */
 SQ_API int sq_version(void);
@@ -160,13 +169,20 @@ SQ_API sq_status sq_smooth_scales_wmax(const float* w_max, const float* act_max,
  * nonfinite_count (device int*, nullable): incremented once per group that holds
  * NaN/Inf after the fold (or whose r/15 exceeds the fp16 range); such a group is
  * stored as scale = 0x7E00 (NaN), zero = 0, codes = 0.
- * s: fp32[K] device or NULL.  Requires group == 128, K % 128 == 0, N % 8 == 0,
- * 16-byte aligned W/Wq/scales/zeros.
+ * s: fp32[K] device or NULL.  Requires group in {32, 64, 128},
+ * K % 128 == 0, N % 8 == 0, 16-byte aligned W/Wq/scales/zeros.
  */
 SQ_API sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s,
                                      int64_t N, int64_t K, int group,
                                      uint8_t* Wq, uint16_t* scales, uint16_t* zeros,
                                      int* nonfinite_count, void* stream);
+/* Same with flags: 0 (== sq_quantize_pack_groupwise) or SQ_ZEROS_U4 -- zeros is then
+ * written as packed uint8[G][N/2] (N % 32 == 0), a non-finite group's Z as 0.  Other
+ * bits -> SQ_ERR_UNSUPPORTED. */
+SQ_API sq_status sq_quantize_pack_groupwise_ex(const void* W, int w_dtype, const float* s,
+                                        int64_t N, int64_t K, int group,
+                                        uint8_t* Wq, uint16_t* scales, void* zeros,
+                                        int* nonfinite_count, unsigned flags, void* stream);
 
 /*
  * Bytes of caller-allocated device workspace sq_w4a16_gemm needs for this shape
@@ -200,8 +216,8 @@ SQ_API sq_status sq_w4a16_gemm(const void* X, int x_dtype,
                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Same as sq_w4a16_gemm with an explicit path (SQ_PATH_*: AUTO, DECODE for M <= 16,
- * PREFILL) and per-call flags (SQ_GEMM_WEIGHTS_STATIC or 0; other bits ->
- * SQ_ERR_UNSUPPORTED).  sq_w4a16_gemm == sq_w4a16_gemm_ex(..., SQ_PATH_AUTO, 0, stream). */
+ * PREFILL) and per-call flags (SQ_GEMM_WEIGHTS_STATIC | SQ_ZEROS_U4 or 0; other bits ->
+ * SQ_ERR_UNSUPPORTED; with SQ_ZEROS_U4 `zeros` points to the packed uint8[G][N/2]).  sq_w4a16_gemm == sq_w4a16_gemm_ex(..., SQ_PATH_AUTO, 0, stream). */
 SQ_API sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype,
                            const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
                            void* Y, int64_t M, int64_t N, int64_t K, int group,

@@ -44,10 +44,9 @@ __device__ __forceinline__ void dequant_word(uint32_t w, uint32_t zsub, uint32_t
   }
 }
 
-// zero-point constants from the fp16 bits of Z (an integer 0..15)
+// zero-point constants from the integer Z (0..15)
 template <bool kBF16>
-__device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint32_t& zfma) {
-  const uint32_t z = (uint32_t)__half2int_rn(__ushort_as_half(zbits));
+__device__ __forceinline__ void zero_consts_q(uint32_t z, uint32_t& zsub, uint32_t& zfma) {
   if (!kBF16) {
     zsub = z * 0x00010001u + 0x64006400u;         // fp16x2(1024 + Z): ulp of 1024 is 1
     zfma = z * 0x00100010u + 0xD400D400u;         // fp16x2(-(64 + Z)): ulp of 64 is 1/16
@@ -55,6 +54,19 @@ __device__ __forceinline__ void zero_consts(uint16_t zbits, uint32_t& zsub, uint
     zsub = z * 0x00010001u + 0x43004300u;         // bf16x2(128 + Z): ulp of 128 is 1
     zfma = 0;
   }
+}
+// Z of weight row `row` in a stage's zero rows: fp16 bits (uint16 per row), or packed u4
+// (SQ_ZEROS_U4: uint8 per row pair, low nibble = even row).  zrow: shared address of the
+// stage's zero row (fp16: row 0's element; u4: row 0's byte).
+__device__ __forceinline__ uint32_t load_zero(uint32_t zrow, int row, bool u4) {
+  if (u4) {
+    uint32_t b;
+    asm("ld.shared.u8 %0, [%1];\n" : "=r"(b) : "r"(zrow + (uint32_t)(row >> 1)) : "memory");
+    return (b >> (4 * (row & 1))) & 0xFu;
+  }
+  uint16_t h;
+  asm("ld.shared.u16 %0, [%1];\n" : "=h"(h) : "r"(zrow + 2u * (uint32_t)row) : "memory");
+  return (uint32_t)__half2int_rn(__ushort_as_half(h));
 }
 
 // Work split.  Units are numbered u = rb * upb + pos (row block rb, stage pos).

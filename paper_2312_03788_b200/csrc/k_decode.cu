@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(Cfg<MT, BN, XR, CT, GS>::THREADS, CT)
 decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
               const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
               uint16_t* __restrict__ Y, int* __restrict__ counters, float* __restrict__ partials,
-              int M, int N, Work wk, int early_weights, const ArParams ar) {
+              int M, int N, Work wk, int early_weights, int zu4, const ArParams ar) {
   using C = Cfg<MT, BN, XR, CT, GS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -272,6 +272,9 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int c = blockIdx.x, P = gridDim.x;
+  // bytes the TMA delivers per stage: packed u4 zero rows (SQ_ZEROS_U4) are a quarter of
+  // the fp16 ones; they land at the start of the same zero-row region, [slot][sub][BN / 2]
+  const uint32_t tx = zu4 ? (uint32_t)(C::TX - C::SZ + C::SZ / 4) : (uint32_t)C::TX;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) {
@@ -299,7 +302,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const int rb = u / wk.upb, g0 = (u % wk.upb) * GPS;
         tma_3d_hint(st, &tm_w, fb, 0, rb * BN, g0, wpol);
         tma_2d(st + C::CODES + C::XB, &tm_s, fb, rb * BN, g0 * C::SUB);
-        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, rb * BN, g0 * C::SUB);
+        tma_2d(st + C::CODES + C::XB + C::SZ, &tm_z, fb, zu4 ? rb * (BN / 2) : rb * BN, g0 * C::SUB);
       };
       // Weights (codes, Δ, Z) never depend on the previous kernel when the caller
       // declared them static (SQ_GEMM_WEIGHTS_STATIC): stream the first stages before
@@ -309,7 +312,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         Sched sc(wk, c, P);
         for (; pre < C::NS && sc.valid(); ++pre, sc.next(wk)) {
           const uint32_t fb = bar_full + 8 * pre;
-          mbar_expect_tx(fb, C::TX);
+          mbar_expect_tx(fb, tx);
           load_weights(sbase + pre * C::STAGE, fb, sc.u);
         }
       }
@@ -322,7 +325,7 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
         const uint32_t fb = bar_full + 8 * s;
         if (i >= pre) {
           mbar_wait_idle(bar_empty + 8 * s, ph ^ 1);
-          mbar_expect_tx(fb, C::TX);
+          mbar_expect_tx(fb, tx);
           load_weights(st, fb, sc.u);
         }
         tma_4d(st + C::CODES, &tm_x, fb, 0, 0, 0, (sc.u % wk.upb) * GPS);
@@ -561,21 +564,23 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
     // codes of this warp's group: [group][row][64 B]
     const uint32_t cbase = st + grp * (BN * 64) + r * 64 + j * 16;
     const uint32_t sbs = st + C::CODES + C::XB + grp * (BN * 2) + r * 2;
-    const uint32_t sbz = sbs + C::SZ;
+    // this warp's group row of the zero region (fp16: BN x 2 B per group, u4: BN / 2 B)
+    const uint32_t zrow = st + C::CODES + C::XB + C::SZ + grp * (zu4 ? BN / 2 : BN * 2);
     if constexpr (GS < kGroup) {
       // groups of 64 / 32 k: one MMA's 16 k span the four lanes' 32-k ranges, i.e. up to
       // four groups, so Δ cannot be applied to the fp32 sum; the operand is the rounded
       // Ŵ = RN((q - Z) Δ) instead (the value the prefill path feeds its MMA, P13) and the
       // MMA accumulates Ŵ·X directly.  Lane j's k range lies in group (32 j) / GS.
       const uint32_t sbg = st + C::CODES + C::XB + ((grp * C::SUB + (32 * j) / GS) * BN + r) * 2;
+      const uint32_t zrow_g = st + C::CODES + C::XB + C::SZ + (grp * C::SUB + (32 * j) / GS) * (zu4 ? BN / 2 : BN * 2);
 #pragma unroll
       for (int rt = 0; rt < C::RT; ++rt) {
         const uint4 ca = lds128(cbase + rt * 16 * 64);
         const uint4 cb = lds128(cbase + (rt * 16 + 8) * 64);
         const uint16_t dA = lds16(sbg + rt * 32), dB = lds16(sbg + rt * 32 + 16);
         uint32_t zsA, zfA, zsB, zfB;
-        zero_consts<kBF16>(lds16(sbg + C::SZ + rt * 32), zsA, zfA);
-        zero_consts<kBF16>(lds16(sbg + C::SZ + rt * 32 + 16), zsB, zfB);
+        zero_consts_q<kBF16>(load_zero(zrow_g, rt * 16 + r, zu4), zsA, zfA);
+        zero_consts_q<kBF16>(load_zero(zrow_g, rt * 16 + r + 8, zu4), zsB, zfB);
         const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
         const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
@@ -602,8 +607,8 @@ decode_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ 
       const uint32_t wa[4] = {ca.x, ca.y, ca.z, ca.w};
       const uint32_t wb[4] = {cb.x, cb.y, cb.z, cb.w};
       uint32_t zsA, zfA, zsB, zfB;
-      zero_consts<kBF16>(lds16(sbz + rt * 32), zsA, zfA);
-      zero_consts<kBF16>(lds16(sbz + rt * 32 + 16), zsB, zfB);
+      zero_consts_q<kBF16>(load_zero(zrow, rt * 16 + r, zu4), zsA, zfA);
+      zero_consts_q<kBF16>(load_zero(zrow, rt * 16 + r + 8, zu4), zsB, zfB);
       float g[MT][4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
@@ -716,9 +721,9 @@ int ctas_per_sm() {
 }
 
 template <int MT, bool kBF16, int BN, int XR, int CT, int GS = 128>
-cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, const void* zeros,
                      void* Y, int M, int N, int K, void* ws, bool dp, const ArParams& ar, bool weights_static,
-                     int grid_per_sm, cudaStream_t st, const char** why) {
+                     bool zu4, int grid_per_sm, cudaStream_t st, const char** why) {
   using C = Cfg<MT, BN, XR, CT, GS>;
   const int G = K / kGroup;  // 128-k slots
   CUtensorMap tw, tx, ts, tz;
@@ -744,8 +749,13 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     const uint64_t d[2] = {(uint64_t)N, (uint64_t)G * C::SUB};  // [K / GS][N]
     const uint64_t s[1] = {(uint64_t)N * 2};
     const uint32_t b[2] = {(uint32_t)BN, (uint32_t)(GPS * C::SUB)};
+    // packed u4 zeros: uint8[K / GS][N / 2], a box of BN / 2 bytes per zero row
+    const uint64_t dz[2] = {(uint64_t)N / 2, (uint64_t)G * C::SUB};
+    const uint64_t sz[1] = {(uint64_t)N / 2};
+    const uint32_t bz[2] = {(uint32_t)BN / 2, (uint32_t)(GPS * C::SUB)};
     if (!encode(&ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, scales, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, zeros, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+        !(zu4 ? encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, zeros, dz, sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE)
+              : encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, zeros, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE))) {
       *why = "tensor map (scales/zeros)";
       return cudaErrorInvalidValue;
     }
@@ -777,9 +787,9 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   const int early = option(SQ_OPT_PDL) && weights_static;
   if (ar.world > 0)
     return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, true, GS>, tw, tx, ts, tz, (uint16_t*)Y,
-                              counters, partials, M, N, wk, early, ar);
+                              counters, partials, M, N, wk, early, zu4 ? 1 : 0, ar);
   return cudaLaunchKernelEx(&cfg, decode_kernel<MT, kBF16, BN, XR, CT, false, GS>, tw, tx, ts, tz, (uint16_t*)Y,
-                            counters, partials, M, N, wk, early, ar);
+                            counters, partials, M, N, wk, early, zu4 ? 1 : 0, ar);
 }
 
 // Fraction of the resident CTA slots kept busy by whole row blocks of height bn.
@@ -806,9 +816,9 @@ bool auto_rowblock(int N, int K, int slots, int* bn_out) {
 }
 
 template <int MT, bool kBF16, int XR, int CT>
-cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
+cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, const void* zeros,
                      void* Y, int M, int N, int K, void* ws, const ArParams& ar, bool weights_static,
-                     cudaStream_t st, const char** why, int grid_per_sm = CT) {
+                     bool zu4, cudaStream_t st, const char** why, int grid_per_sm = CT) {
   const int sched = option(SQ_OPT_DECODE_SCHEDULE);
   const int slots = num_sms() * grid_per_sm;
   // AUTO (measured on the 34B and 7B shapes, 48-launch chains): whole row
@@ -840,9 +850,9 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     bn = 64;
   }
   if (bn == 32)
-    return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, grid_per_sm,
+    return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4, grid_per_sm,
                                            st, why);
-  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, grid_per_sm, st,
+  return launch_t<MT, kBF16, 64, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4, grid_per_sm, st,
                                          why);
 }
 
@@ -864,35 +874,35 @@ size_t decode_workspace_bytes(int64_t N) {
 
 template <int GS>
 cudaError_t launch_small_group(const void* X, bool bf16, const uint8_t* Wq, const uint16_t* scales,
-                               const uint16_t* zeros, void* Y, int M, int N, int K, void* ws, const ArParams& ar,
-                               bool weights_static, cudaStream_t st, const char** why) {
+                               const void* zeros, void* Y, int M, int N, int K, void* ws, const ArParams& ar,
+                               bool weights_static, bool zu4, cudaStream_t st, const char** why) {
   // group sizes 64 / 32: one configuration per M class (stream-K, 64-row blocks, two CTAs per SM)
   constexpr int C2 = kCtasPerSm;
   if (M == 1)
-    return bf16 ? launch_t<1, true, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+    return bf16 ? launch_t<1, true, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4, C2,
                                                    st, why)
-                : launch_t<1, false, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static,
+                : launch_t<1, false, 64, 1, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4,
                                                     C2, st, why);
   if (M <= 8)
-    return bf16 ? launch_t<1, true, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+    return bf16 ? launch_t<1, true, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4, C2,
                                                    st, why)
-                : launch_t<1, false, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static,
+                : launch_t<1, false, 64, 8, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4,
                                                     C2, st, why);
-  return bf16 ? launch_t<2, true, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+  return bf16 ? launch_t<2, true, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4, C2,
                                                   st, why)
-              : launch_t<2, false, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, C2,
+              : launch_t<2, false, 64, 16, C2, GS>(X, Wq, scales, zeros, Y, M, N, K, ws, false, ar, weights_static, zu4, C2,
                                                    st, why);
 }
 
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws,
-                          bool weights_static, cudaStream_t st, const char** why, const ArParams* ar_in) {
+                          const void* zeros, void* Y, int M, int N, int K, int group, void* ws,
+                          bool weights_static, bool zu4, cudaStream_t st, const char** why, const ArParams* ar_in) {
   const ArParams ar = ar_in ? *ar_in : ArParams{nullptr, 0, nullptr, 0, 0, 0u};
   const bool bf16 = x_dtype == SQ_BF16;
   if (group == 64)
-    return launch_small_group<64>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+    return launch_small_group<64>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   if (group == 32)
-    return launch_small_group<32>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+    return launch_small_group<32>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
     // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
     // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
@@ -902,16 +912,16 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
     int rbn = 64;
     if (ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO && codes >= 32.0 * 1024 * 1024 &&
         codes <= 64.0 * 1024 * 1024 && !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn))
-      return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
-                  : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
-    return bf16 ? launch_m<1, true, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
-                : launch_m<1, false, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+      return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+                  : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
+    return bf16 ? launch_m<1, true, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+                : launch_m<1, false, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   }
   if (M <= 8)
-    return bf16 ? launch_m<1, true, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
-                : launch_m<1, false, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
-  return bf16 ? launch_m<2, true, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why)
-              : launch_m<2, false, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, st, why);
+    return bf16 ? launch_m<1, true, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+                : launch_m<1, false, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
+  return bf16 ? launch_m<2, true, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+              : launch_m<2, false, 16, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
 }
 
 }  // namespace sq

@@ -221,6 +221,11 @@ __device__ __forceinline__ uint16_t lds16(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups
 // 1024 bytes apart (SBO), sm_100 descriptor version 1.
@@ -334,7 +339,8 @@ __global__ void __launch_bounds__(PCfg<kBT>::THREADS, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
                uint16_t* __restrict__ Y, int M, int N, int K, int early_weights, int x_bytes,
-               int sk, int cta_q, int cta_r, float* __restrict__ partials, int* __restrict__ counters) {
+               int sk, int cta_q, int cta_r, float* __restrict__ partials, int* __restrict__ counters,
+               int zu4) {
   using C = PCfg<kBT>;
   constexpr int BT = C::BT, KA = C::KA, APS = C::APS, R = C::R, DQW = C::DQW;
   constexpr int NSX = C::NSX, NSC = C::NSC, NSA = C::NSA;
@@ -418,10 +424,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         const int n0 = (tile / m_tiles) * BM;
         for (int g = sc.g0; g < sc.g1; ++g) {
           mbar_wait(c_empty(cs), cph ^ 1);
-          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + 2 * SUBS * BM * 2);
+          // packed u4 zero rows (SQ_ZEROS_U4) are BM / 2 bytes, at the start of the same slot
+          mbar_expect_tx(c_full(cs), C_STAGE_BYTES + SUBS * BM * 2 + (zu4 ? SUBS * BM / 2 : SUBS * BM * 2));
           tma_load_2d(sbase + C::OFF_C + cs * C_STAGE_BYTES, &tm_w, c_full(cs), g * (kGroup / 2), n0);
           tma_load_2d(sbase + C::OFF_S + cs * SZ_BYTES, &tm_s, c_full(cs), n0, g * SUBS);
-          tma_load_2d(sbase + C::OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), n0, g * SUBS);
+          tma_load_2d(sbase + C::OFF_Z + cs * SZ_BYTES, &tm_z, c_full(cs), zu4 ? n0 / 2 : n0, g * SUBS);
           if (++cs == NSC) { cs = 0; cph ^= 1; }
         }
       }
@@ -485,12 +492,16 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         }
         constexpr int NG = KA >= GS ? KA / GS : 1;  // quantization groups in the A stage
         constexpr int GSPAN = KA >= GS ? GS : KA;   // k of the A stage in each
-        uint16_t sbits[NG], zbits[NG];
+        uint16_t sbits[NG];
+        uint32_t zq[NG];  // Z (integer 0..15) from fp16 bits or a packed u4 nibble
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
           const int sub = (t * KA + h * GSPAN) / GS;
           sbits[h] = lds16(sbase + C::OFF_S + cs * SZ_BYTES + (sub * BM + row) * 2);
-          zbits[h] = lds16(sbase + C::OFF_Z + cs * SZ_BYTES + (sub * BM + row) * 2);
+          if (zu4)
+            zq[h] = (lds8(sbase + C::OFF_Z + cs * SZ_BYTES + sub * (BM / 2) + (row >> 1)) >> (4 * (row & 1))) & 0xFu;
+          else
+            zq[h] = (uint32_t)__half2int_rn(__ushort_as_half(lds16(sbase + C::OFF_Z + cs * SZ_BYTES + (sub * BM + row) * 2)));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(c_empty(cs));
@@ -499,9 +510,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         bool sat = false;  // fp16 groups with Δ > 65504 / 15 take the saturating conversion
 #pragma unroll
         for (int h = 0; h < NG; ++h) {
-          const __half2 zc2 = __half2half2(__hadd(__float2half(1024.0f), __ushort_as_half(zbits[h])));
           const __half2 d2h = __half2half2(__ushort_as_half(sbits[h]));
-          zc[h] = *reinterpret_cast<const uint32_t*>(&zc2);
+          zc[h] = (0x6400u + zq[h]) * 0x00010001u;  // fp16x2(1024 + Z): ulp of 1024 is 1
           d2[h] = *reinterpret_cast<const uint32_t*>(&d2h);
           df[h] = __half2float(__ushort_as_half(sbits[h]));
           sat |= !kBF16 && df[h] > 4366.0f;
@@ -683,9 +693,9 @@ auto pick_kernel(int group) {
 }
 
 template <int kBT>
-cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales, const uint16_t* zeros,
-                      void* Y, int M, int N, int K, int group, void* ws, bool weights_static, cudaStream_t st,
-                      const char** why) {
+cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales, const void* zeros,
+                      void* Y, int M, int N, int K, int group, void* ws, bool weights_static, bool zu4,
+                      cudaStream_t st, const char** why) {
   using C = PCfg<kBT>;
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = (int)prefill_stages(M, K);
@@ -700,8 +710,10 @@ cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint1
   const int subs = sub;
   ok = ok && encode_2d(&tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT16, scales, (uint64_t)N, (uint64_t)(K / kGroup) * sub,
                        (uint64_t)N * 2, BM, subs, CU_TENSOR_MAP_SWIZZLE_NONE);
-  ok = ok && encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)(K / kGroup) * sub,
-                       (uint64_t)N * 2, BM, subs, CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok = ok && (zu4 ? encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT8, zeros, (uint64_t)N / 2,
+                              (uint64_t)(K / kGroup) * sub, (uint64_t)N / 2, BM / 2, subs, CU_TENSOR_MAP_SWIZZLE_NONE)
+                  : encode_2d(&tm_z, CU_TENSOR_MAP_DATA_TYPE_UINT16, zeros, (uint64_t)N, (uint64_t)(K / kGroup) * sub,
+                              (uint64_t)N * 2, BM, subs, CU_TENSOR_MAP_SWIZZLE_NONE));
   if (!ok) {
     *why = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
@@ -728,22 +740,22 @@ cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint1
   cfg.numAttrs = 1;
   const int early = option(SQ_OPT_PDL) && weights_static;
   e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, tm_s, tm_z, (uint16_t*)Y, M, N, K, early,
-                         x_rows * C::KA * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters);
+                         x_rows * C::KA * 2, sk ? 1 : 0, cta_q, cta_r, partials, counters, zu4 ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws, size_t,
-                           bool weights_static, cudaStream_t st, const char** why) {
+                           const void* zeros, void* Y, int M, int N, int K, int group, void* ws, size_t,
+                           bool weights_static, bool zu4, cudaStream_t st, const char** why) {
   switch (prefill_bt(M)) {
     case 64:
-      return launch_bt<64>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+      return launch_bt<64>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
     case 128:
-      return launch_bt<128>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+      return launch_bt<128>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
     default:
-      return launch_bt<kBTMax>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, st, why);
+      return launch_bt<kBTMax>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
   }
 }
 

@@ -87,7 +87,7 @@ template <bool kBF16, int GS>
 __global__ void __launch_bounds__(kThreads)
 quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int N, int K, int NSL,
                 uint8_t* __restrict__ Wq, uint16_t* __restrict__ scales,
-                uint16_t* __restrict__ zeros, int* __restrict__ nonfinite) {
+                void* __restrict__ zeros, int zeros_u4, int* __restrict__ nonfinite) {
   constexpr int kLanesPerGroup = GS / 16;
   const int sub = threadIdx.x % kLanesPerSlot;
   const int n = blockIdx.y * kRowsPerCta + threadIdx.x / kLanesPerSlot;
@@ -204,13 +204,20 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
         }
       }
     }
+    // packed u4 Z (SQ_ZEROS_U4): rows n and n + 1 of a pair sit 8 lanes apart in the warp
+    // (8 lanes per row); the even row's lane writes the byte, low nibble = even n
+    const uint32_t zq = nf ? 0u : (uint32_t)z;
+    const uint32_t zq_odd = __shfl_down_sync(0xffffffffu, zq, kLanesPerSlot);
     if (row_ok) {
       *reinterpret_cast<uint2*>(Wq + (size_t)n * (K / 2) + (size_t)g * (kSlot / 2) + sub * 8) =
           make_uint2(packed[0], packed[1]);
       if (sub % kLanesPerGroup == 0) {  // first lane of each group
         const size_t gi = (size_t)g * (kSlot / GS) + sub / kLanesPerGroup;
         scales[gi * N + n] = nf ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(d));
-        zeros[gi * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
+        if (!zeros_u4)
+          reinterpret_cast<uint16_t*>(zeros)[gi * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
+        else if ((n & 1) == 0)
+          reinterpret_cast<uint8_t*>(zeros)[gi * (N / 2) + n / 2] = (uint8_t)(zq | (zq_odd << 4));
         if (nf && nonfinite != nullptr) atomicAdd(nonfinite, 1);
       }
     }
@@ -221,26 +228,26 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
 
 template <int GS>
 void launch_gs(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, uint8_t* Wq, uint16_t* scales,
-               uint16_t* zeros, int* nonfinite, cudaStream_t st) {
+               void* zeros, bool zu4, int* nonfinite, cudaStream_t st) {
   const int NSL = (int)(K / kSlot);
   dim3 grid((unsigned)((NSL + kSlotsPerCta - 1) / kSlotsPerCta), (unsigned)((N + kRowsPerCta - 1) / kRowsPerCta));
   if (w_dtype == SQ_BF16)
     quantize_kernel<true, GS><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, NSL, Wq, scales,
-                                                         zeros, nonfinite);
+                                                         zeros, zu4 ? 1 : 0, nonfinite);
   else
     quantize_kernel<false, GS><<<grid, kThreads, 0, st>>>((const uint16_t*)W, s, (int)N, (int)K, NSL, Wq, scales,
-                                                          zeros, nonfinite);
+                                                          zeros, zu4 ? 1 : 0, nonfinite);
 }
 
 cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, int group,
-                            uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
+                            uint8_t* Wq, uint16_t* scales, void* zeros, bool zeros_u4, int* nonfinite,
                             cudaStream_t st) {
   if (group == 32)
-    launch_gs<32>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
+    launch_gs<32>(W, w_dtype, s, N, K, Wq, scales, zeros, zeros_u4, nonfinite, st);
   else if (group == 64)
-    launch_gs<64>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
+    launch_gs<64>(W, w_dtype, s, N, K, Wq, scales, zeros, zeros_u4, nonfinite, st);
   else
-    launch_gs<128>(W, w_dtype, s, N, K, Wq, scales, zeros, nonfinite, st);
+    launch_gs<128>(W, w_dtype, s, N, K, Wq, scales, zeros, zeros_u4, nonfinite, st);
   return cudaGetLastError();
 }
 

@@ -168,16 +168,24 @@ sq_status sq_smooth_scales_wmax(const float* w_max, const float* act_max, int64_
 sq_status sq_quantize_pack_groupwise(const void* W, int w_dtype, const float* s, int64_t N,
                                      int64_t K, int group, uint8_t* Wq, uint16_t* scales,
                                      uint16_t* zeros, int* nonfinite_count, void* stream) {
+  return sq_quantize_pack_groupwise_ex(W, w_dtype, s, N, K, group, Wq, scales, zeros, nonfinite_count, 0u, stream);
+}
+
+sq_status sq_quantize_pack_groupwise_ex(const void* W, int w_dtype, const float* s, int64_t N,
+                                        int64_t K, int group, uint8_t* Wq, uint16_t* scales,
+                                        void* zeros, int* nonfinite_count, unsigned flags, void* stream) {
   g_last_error.clear();
+  if (flags & ~(unsigned)SQ_ZEROS_U4) return fail(SQ_ERR_UNSUPPORTED, "sq_quantize_pack_groupwise: flags 0x%x", flags);
+  const bool zu4 = (flags & SQ_ZEROS_U4) != 0;
   if (!W || !Wq || !scales || !zeros) return fail(SQ_ERR_NULL, "sq_quantize_pack_groupwise: null pointer");
   if (N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: N=%lld K=%lld", (long long)N, (long long)K);
   if (!valid_group(group) || K % 128 != 0 || !valid_dtype(w_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_quantize_pack_groupwise: group=%d K=%lld dtype=%d", group, (long long)K, w_dtype);
   if (N % 8 != 0 || !aligned16(W) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
-      (s && !aligned16(s)))
-    return fail(SQ_ERR_ALIGN, "sq_quantize_pack_groupwise: N %% 8 != 0 or unaligned pointer");
+      (s && !aligned16(s)) || (zu4 && N % 32 != 0))
+    return fail(SQ_ERR_ALIGN, "sq_quantize_pack_groupwise: N %% 8 != 0 (N %% 32 with u4 zeros) or unaligned pointer");
   if (N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_quantize_pack_groupwise: too large");
-  return cuda_status(launch_quantize(W, w_dtype, s, N, K, group, Wq, scales, zeros, nonfinite_count,
+  return cuda_status(launch_quantize(W, w_dtype, s, N, K, group, Wq, scales, zeros, zu4, nonfinite_count,
                                      (cudaStream_t)stream), "quantize");
 }
 
@@ -204,10 +212,12 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
   if (M < 0 || N <= 0 || K <= 0) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
   if (!valid_group(group) || K % 128 != 0 || !valid_dtype(x_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
-  if (flags & ~(unsigned)SQ_GEMM_WEIGHTS_STATIC) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: flags 0x%x", flags);
+  if (flags & ~(unsigned)(SQ_GEMM_WEIGHTS_STATIC | SQ_ZEROS_U4))
+    return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm: flags 0x%x", flags);
+  const bool zu4 = (flags & SQ_ZEROS_U4) != 0;
   if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) ||
-      !aligned16(Y))
-    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm: N %% 8 != 0 or unaligned pointer");
+      !aligned16(Y) || (zu4 && N % 32 != 0))
+    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm: N %% 8 != 0 (N %% 32 with u4 zeros) or unaligned pointer");
   if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30)) return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm: too large");
   const bool wstatic = (flags & SQ_GEMM_WEIGHTS_STATIC) != 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -219,7 +229,7 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: decode needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
     cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group, workspace, wstatic,
-                                  st, &why);
+                                  zu4, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm decode: %s", why);
     return cuda_status(e, "decode");
   }
@@ -229,7 +239,7 @@ sq_status sq_w4a16_gemm_ex(const void* X, int x_dtype, const uint8_t* Wq, const 
       return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm: prefill needs %zu workspace bytes (16-byte aligned)", need);
     const char* why = nullptr;
     cudaError_t e = launch_prefill(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group,
-                                   workspace, workspace_bytes, wstatic, st, &why);
+                                   workspace, workspace_bytes, wstatic, zu4, st, &why);
     if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm prefill: %s", why);
     return cuda_status(e, "prefill");
   }
@@ -299,8 +309,9 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
                                   int world, int64_t n_max, uint32_t epoch, int* error_flag, unsigned flags,
                                   void* stream) {
   g_last_error.clear();
-  if (flags & ~(unsigned)SQ_GEMM_WEIGHTS_STATIC)
+  if (flags & ~(unsigned)(SQ_GEMM_WEIGHTS_STATIC | SQ_ZEROS_U4))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: flags 0x%x", flags);
+  const bool zu4 = (flags & SQ_ZEROS_U4) != 0;
   if (world <= 0 || rank < 0 || rank >= world || M < 0 || N <= 0 || M * N > n_max)
     return fail(SQ_ERR_SHAPE, "sq_w4a16_gemm_allreduce: M=%lld N=%lld n_max=%lld rank=%d world=%d", (long long)M,
                 (long long)N, (long long)n_max, rank, world);
@@ -322,15 +333,16 @@ sq_status sq_w4a16_gemm_allreduce(const void* X, int x_dtype, const uint8_t* Wq,
   if (!X || !Wq || !scales || !zeros || !Y) return fail(SQ_ERR_NULL, "sq_w4a16_gemm_allreduce: null pointer");
   if (K <= 0 || !valid_group(group) || K % 128 != 0 || !valid_dtype(x_dtype))
     return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: group=%d K=%lld dtype=%d", group, (long long)K, x_dtype);
-  if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) || !aligned16(Y))
-    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: N %% 8 != 0 or unaligned pointer");
+  if (N % 8 != 0 || !aligned16(X) || !aligned16(Wq) || !aligned16(scales) || !aligned16(zeros) || !aligned16(Y) ||
+      (zu4 && N % 32 != 0))
+    return fail(SQ_ERR_ALIGN, "sq_w4a16_gemm_allreduce: N %% 8 != 0 (N %% 32 with u4 zeros) or unaligned pointer");
   const size_t need = decode_workspace_bytes(N);
   if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
     return fail(SQ_ERR_WORKSPACE, "sq_w4a16_gemm_allreduce: decode needs %zu workspace bytes", need);
   const ArParams ar{reinterpret_cast<uint8_t* const*>(peer_bufs), n_max, error_flag, rank, world, epoch};
   const char* why = nullptr;
   cudaError_t e = launch_decode(X, x_dtype, Wq, scales, zeros, Y, (int)M, (int)N, (int)K, group, workspace,
-                                (flags & SQ_GEMM_WEIGHTS_STATIC) != 0, (cudaStream_t)stream, &why, &ar);
+                                (flags & SQ_GEMM_WEIGHTS_STATIC) != 0, zu4, (cudaStream_t)stream, &why, &ar);
   if (why) return fail(SQ_ERR_UNSUPPORTED, "sq_w4a16_gemm_allreduce: %s", why);
   return cuda_status(e, "sq_w4a16_gemm_allreduce");
 }

@@ -15,9 +15,10 @@ cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K,
                              float* out_bits_as_float, cudaStream_t st);
 cudaError_t launch_smooth_finalize(const float* act_max, float* s_inout, int64_t K,
                                    double alpha, double eps, cudaStream_t st);
-// group: 32, 64 or 128 (K % 128 == 0)
+// group: 32, 64 or 128 (K % 128 == 0).  zeros_u4: Z packed two per byte along n
+// (uint8[G][N/2], low nibble = even n) instead of fp16 bits uint16[G][N] (SQ_ZEROS_U4).
 cudaError_t launch_quantize(const void* W, int w_dtype, const float* s, int64_t N, int64_t K, int group,
-                            uint8_t* Wq, uint16_t* scales, uint16_t* zeros, int* nonfinite,
+                            uint8_t* Wq, uint16_t* scales, void* zeros, bool zeros_u4, int* nonfinite,
                             cudaStream_t st);
 
 // GEMM workspace layout: [fp32 partial tiles: ws_partials_bytes()][int counters].  The
@@ -45,15 +46,18 @@ struct ArParams {
 // weights_static: the caller promised (SQ_GEMM_WEIGHTS_STATIC) that the weights are not
 // written by the preceding kernels, so with PDL the weight loads may start before the
 // previous kernel has finished.
+// zeros_u4: zeros is uint8[G][N/2] (two 4-bit Z per byte along n, SQ_ZEROS_U4), else
+// fp16 bits uint16[G][N].
 cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                          const uint16_t* zeros, void* Y, int M, int N, int K, int group, void* ws,
-                          bool weights_static, cudaStream_t st, const char** why, const ArParams* ar = nullptr);
+                          const void* zeros, void* Y, int M, int N, int K, int group, void* ws,
+                          bool weights_static, bool zeros_u4, cudaStream_t st, const char** why,
+                          const ArParams* ar = nullptr);
 
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales,
-                           const uint16_t* zeros, void* Y, int M, int N, int K, int group,
-                           void* workspace, size_t ws_bytes, bool weights_static, cudaStream_t st,
-                           const char** why);
+                           const void* zeros, void* Y, int M, int N, int K, int group,
+                           void* workspace, size_t ws_bytes, bool weights_static, bool zeros_u4,
+                           cudaStream_t st, const char** why);
 
 int num_sms();
 int option(int opt);

@@ -31,6 +31,7 @@ SQ_F16, SQ_BF16 = 0, 1
 SQ_PATH_AUTO, SQ_PATH_DECODE, SQ_PATH_PREFILL = 0, 1, 2
 SQ_OPT_PDL, SQ_OPT_DECODE_SCHEDULE, SQ_OPT_DECODE_GRID_LIMIT = 1, 3, 5
 SQ_GEMM_WEIGHTS_STATIC = 1
+SQ_ZEROS_U4 = 2
 SQ_SCHED_AUTO, SQ_SCHED_STREAMK, SQ_SCHED_ROWBLOCK = 0, 1, 2
 GROUP = 128
 
@@ -64,6 +65,7 @@ def _load():
         "sq_smooth_scales_wmax": (i32, [vp, vp, i64, f64, f64, vp, vp]),
         "sq_workspace_reset": (i32, [vp, sz, vp]),
         "sq_quantize_pack_groupwise": (i32, [vp, i32, vp, i64, i64, i32, vp, vp, vp, vp, vp]),
+        "sq_quantize_pack_groupwise_ex": (i32, [vp, i32, vp, i64, i64, i32, vp, vp, vp, vp, c.c_uint, vp]),
         "sq_w4a16_gemm_workspace_bytes": (sz, [i64, i64, i64, i32]),
         "sq_w4a16_gemm": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, vp]),
         "sq_w4a16_gemm_path": (i32, [vp, i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, sz, i32, vp]),
@@ -92,7 +94,8 @@ def _load():
 EXPORTED = (
     "sq_version", "sq_status_string", "sq_last_error", "sq_decode_max_m", "sq_set_option",
     "sq_get_option", "sq_act_absmax",
-    "sq_smooth_scales", "sq_smooth_scales_wmax", "sq_quantize_pack_groupwise", "sq_w4a16_gemm_workspace_bytes",
+    "sq_smooth_scales", "sq_smooth_scales_wmax", "sq_quantize_pack_groupwise", "sq_quantize_pack_groupwise_ex",
+    "sq_w4a16_gemm_workspace_bytes",
     "sq_workspace_reset", "sq_w4a16_gemm", "sq_w4a16_gemm_path", "sq_w4a16_gemm_ex", "sq_smooth_activations", "sq_sq_diff_sum_workspace_bytes",
     "sq_sq_diff_sum", "sq_fold_rows", "sq_allreduce_buffer_bytes", "sq_w4a16_gemm_allreduce", "sq_allreduce_oneshot", "sq_ipc_handle_bytes",
     "sq_ipc_get_handle", "sq_ipc_open_handle", "sq_ipc_close",
@@ -218,7 +221,8 @@ def smooth_scales_wmax(w_max: torch.Tensor, act_max: torch.Tensor, alpha: float,
 
 @dataclass
 class QuantizedLinear:
-    """W4 g128 weight: codes [N][K/2] u8, scales/zeros [G][N] fp16 bits (as int16 tensors).
+    """W4 weight: codes [N][K/2] u8, scales [G][N] fp16 bits (int16 tensor), zeros [G][N]
+    fp16 bits (int16) or, with zeros_u4, packed uint8 [G][N/2] (SQ_ZEROS_U4).
 
     static: the weights are final (inference).  GEMMs on this handle then pass
     SQ_GEMM_WEIGHTS_STATIC, letting the kernel stream its first weight stages before the
@@ -232,6 +236,7 @@ class QuantizedLinear:
     K: int
     group: int = GROUP
     static: bool = False
+    zeros_u4: bool = False
 
     def mark_static(self, static: bool = True) -> "QuantizedLinear":
         self.static = static
@@ -239,15 +244,17 @@ class QuantizedLinear:
 
     @property
     def flags(self) -> int:
-        return SQ_GEMM_WEIGHTS_STATIC if self.static else 0
+        return (SQ_GEMM_WEIGHTS_STATIC if self.static else 0) | (SQ_ZEROS_U4 if self.zeros_u4 else 0)
 
     def nbytes(self) -> int:
-        return self.Wq.numel() + 2 * self.scales.numel() + 2 * self.zeros.numel()
+        return self.Wq.numel() + 2 * self.scales.numel() + self.zeros.numel() * self.zeros.element_size()
 
 
 def quantize_pack_groupwise(W: torch.Tensor, s: torch.Tensor | None = None, group: int = GROUP,
-                            nonfinite: torch.Tensor | None = None, stream=None) -> QuantizedLinear:
-    """Eq. 5 fold (W' = RN(W·s)) + Eq. 1 group-wise INT4 quantization and packing."""
+                            nonfinite: torch.Tensor | None = None, stream=None,
+                            zeros_u4: bool = False) -> QuantizedLinear:
+    """Eq. 5 fold (W' = RN(W·s)) + Eq. 1 group-wise INT4 quantization and packing;
+    zeros_u4: Z packed two per byte along n (SQ_ZEROS_U4, N % 32 == 0)."""
     _need_cuda(W, s, nonfinite)
     N, K = W.shape
     dev = W.device
@@ -256,10 +263,14 @@ def quantize_pack_groupwise(W: torch.Tensor, s: torch.Tensor | None = None, grou
         raise ValueError("nonfinite: need an int32 device counter")
     Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=dev)
     scales = torch.empty((K // group, N), dtype=torch.int16, device=dev)
-    zeros = torch.empty((K // group, N), dtype=torch.int16, device=dev)
-    _check(_load().sq_quantize_pack_groupwise(_ptr(W), _dtype_code(W), _ptr(s), N, K, group, _ptr(Wq),
-                                              _ptr(scales), _ptr(zeros), _ptr(nonfinite), _stream(stream)))
-    return QuantizedLinear(Wq, scales, zeros, N, K, group)
+    if zeros_u4:
+        zeros = torch.empty((K // group, N // 2), dtype=torch.uint8, device=dev)
+    else:
+        zeros = torch.empty((K // group, N), dtype=torch.int16, device=dev)
+    _check(_load().sq_quantize_pack_groupwise_ex(_ptr(W), _dtype_code(W), _ptr(s), N, K, group, _ptr(Wq),
+                                                 _ptr(scales), _ptr(zeros), _ptr(nonfinite),
+                                                 SQ_ZEROS_U4 if zeros_u4 else 0, _stream(stream)))
+    return QuantizedLinear(Wq, scales, zeros, N, K, group, zeros_u4=zeros_u4)
 
 
 def w4a16_gemm_workspace_bytes(M: int, N: int, K: int, group: int = GROUP) -> int:

@@ -80,6 +80,10 @@ def test_quantize_argument_errors(L):
     assert q(FAKE, 3, None, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_UNSUPPORTED
     assert q(FAKE, 0, None, 12, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
     assert q(FAKE, 0, FAKE_MIS, 8, 256, 128, FAKE, FAKE, FAKE, None, None) == sq.SQ_ERR_ALIGN
+    qx = L.sq_quantize_pack_groupwise_ex      # flags: SQ_ZEROS_U4 only; packed zeros need N % 32 == 0
+    assert qx(FAKE, 0, None, 8, 256, 128, FAKE, FAKE, FAKE, None, 4, None) == sq.SQ_ERR_UNSUPPORTED
+    assert qx(FAKE, 0, None, 40, 256, 128, FAKE, FAKE, FAKE, None, sq.SQ_ZEROS_U4, None) == sq.SQ_ERR_ALIGN
+    assert qx(None, 0, None, 64, 256, 128, FAKE, FAKE, FAKE, None, sq.SQ_ZEROS_U4, None) == sq.SQ_ERR_NULL
 
 
 def test_smooth_argument_errors(L):
@@ -167,7 +171,8 @@ def test_gemm_allreduce_argument_errors(L):
     assert call(err=None) == sq.SQ_ERR_NULL
     assert call(n_max=1028) == sq.SQ_ERR_ALIGN
     assert call(g=16) == sq.SQ_ERR_UNSUPPORTED
-    assert call(flags=2) == sq.SQ_ERR_UNSUPPORTED   # unknown flag bit
+    assert call(flags=4) == sq.SQ_ERR_UNSUPPORTED   # unknown flag bit
+    assert call(flags=sq.SQ_ZEROS_U4, N=264, n_max=2048) == sq.SQ_ERR_ALIGN   # u4 zeros: N % 32
     assert call(M=0) == sq.SQ_OK
 
 
@@ -177,6 +182,9 @@ def test_gemm_ex_flags_and_options(L):
     args = (FAKE, 0, FAKE, FAKE, FAKE, FAKE, 0, 256, 512, 128, None, 0, 0)
     assert f(*args, sq.SQ_GEMM_WEIGHTS_STATIC, None) == sq.SQ_OK      # M = 0: no-op
     assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 256, 512, 128, None, 0, 0, 4, None) == sq.SQ_ERR_UNSUPPORTED
+    # SQ_ZEROS_U4: packed zeros need N % 32 == 0 (16-byte TMA rows)
+    assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 264, 512, 128, None, 0, 0, sq.SQ_ZEROS_U4, None) == sq.SQ_ERR_ALIGN
+    assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 256, 512, 128, None, 0, 1, sq.SQ_ZEROS_U4, None) == sq.SQ_ERR_WORKSPACE
     assert f(FAKE, 0, FAKE, FAKE, FAKE, FAKE, 4, 256, 512, 128, None, 0, 1, 1, None) == sq.SQ_ERR_WORKSPACE
     assert L.sq_set_option(2, 1) == sq.SQ_ERR_UNSUPPORTED            # removed process-wide switch
     assert L.sq_set_option(4, 1) == sq.SQ_ERR_UNSUPPORTED            # removed tcgen05-decode switch

@@ -77,10 +77,11 @@ def test_oneshot_in_place_and_timeout():
     assert int(err.item()) == 1
 
 
+@pytest.mark.parametrize("zeros_u4", [False, True])
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("M", [1, 5, 16])
 @pytest.mark.parametrize("N,K", [(1024, 1024), (2048, 2048), (1024, 3072)])
-def test_fused_gemm_allreduce_streams(M, N, K, dtype):
+def test_fused_gemm_allreduce_streams(M, N, K, dtype, zeros_u4):
     """sq_w4a16_gemm_allreduce (decode: one kernel) for two ranks on two streams of one GPU
     (grids of <= 148 CTAs, so both kernels are resident together), over back-to-back calls
     (both epoch parities, device-managed epoch).  Every rank gets the bit-identical Y, equal
@@ -96,7 +97,7 @@ def test_fused_gemm_allreduce_streams(M, N, K, dtype):
     W_np = synth.weights(N, K, seed=N + K)
     W = torch.from_numpy(W_np).to(DEV)
     ranges = tp.channel_split(K, world)
-    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous()) for a, b in ranges]
+    qs = [sq.quantize_pack_groupwise(W[:, a:b].contiguous(), zeros_u4=zeros_u4) for a, b in ranges]
     full = oracle.quantize_pack(W_np, None)
     W_hat = oracle.dequant(full["Wq"], full["scales"], full["zeros"])
     n_max = M * N

@@ -89,7 +89,10 @@ def _check_quant(W_np, s_np, q: sq.QuantizedLinear, w_dtype="f16", nonfinite=Non
     ref = oracle.quantize_pack(W_np, s_np, group, w_dtype)
     assert (q.Wq.cpu().numpy() == ref["Wq"]).all()
     assert (_bits16(q.scales) == ref["scales"]).all()
-    assert (_bits16(q.zeros) == ref["zeros"]).all()
+    if q.zeros_u4:
+        assert (q.zeros.cpu().numpy() == oracle.pack_zeros_u4(ref["zeros"])).all()
+    else:
+        assert (_bits16(q.zeros) == ref["zeros"]).all()
     if nonfinite is not None:
         assert int(nonfinite.item()) == ref["nonfinite"]
 
@@ -159,7 +162,7 @@ class GemmCase:
         return err
 
 
-def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0, group=128):
+def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0, group=128, zeros_u4=False):
     if W is None:
         W = synth.weights(N, K, seed=seed + 100, heavy=True)
     s = None
@@ -167,7 +170,7 @@ def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0, g
         am = oracle.act_absmax(synth.activations(2048, K, seed=seed + 200).astype(np.float16))
         s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
     ref_q = oracle.quantize_pack(W, s, group)
-    q = sq.quantize_pack_groupwise(_t(W), None if s is None else _t(s), group=group)
+    q = sq.quantize_pack_groupwise(_t(W), None if s is None else _t(s), group=group, zeros_u4=zeros_u4)
     X = synth.activations(M, K, seed=seed + 300, outlier_seed=seed + 200) * x_scale
     if s is not None:  # a5: X̂ = X diag(s)^-1, rounded once to the activation dtype
         X = X.astype(np.float64) / s.astype(np.float64)[None, :]
@@ -179,10 +182,13 @@ def _gemm_case(M, N, K, dtype, path, seed=0, smooth=True, W=None, x_scale=1.0, g
     y = sq.w4a16_gemm(x, q, workspace=ws, path=path)
     torch.cuda.synchronize()
     xn, xd = _x_np_for(x)
-    y_ref = oracle.gemm(xn, ref_q["Wq"], ref_q["scales"], ref_q["zeros"], group, xd)
-    W_hat = oracle.dequant(ref_q["Wq"], ref_q["scales"], ref_q["zeros"], group)
+    zref = oracle.pack_zeros_u4(ref_q["zeros"]) if zeros_u4 else ref_q["zeros"]
+    y_ref = oracle.gemm(xn, ref_q["Wq"], ref_q["scales"], zref, group, xd, zeros_u4=zeros_u4)
+    W_hat = oracle.dequant(ref_q["Wq"], ref_q["scales"], zref, group, zeros_u4=zeros_u4)
     x64 = x.float().cpu().double().numpy()
-    return GemmCase(y, y_ref, x64, W_hat, xd)
+    c = GemmCase(y, y_ref, x64, W_hat, xd)
+    c.q, c.x, c.ws = q, x, ws
+    return c
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
@@ -405,3 +411,42 @@ def test_gemm_group_sizes_parity(path, M, N, K, group, dtype):
     mma.sync, prefill to tcgen05), ragged row blocks and 128-k stages, stream-K fixups,
     against the oracle element by element."""
     _gemm_case(M, N, K, dtype, path, seed=M + group, group=group).check(dtype)
+
+
+# ------------------------------------------------------------------ N3: packed u4 zero points
+@pytest.mark.parametrize("group", [128, 64, 32])
+def test_quantize_zeros_u4_bitexact(group):
+    """SQ_ZEROS_U4: the quantizer writes Z packed two
+    per byte along n, equal to oracle.pack_zeros_u4 of the oracle's fp16 Z, codes and Δ
+    unchanged -- on smoothed weights, the edge-group suite and a non-finite group (Z = 0)."""
+    N, K = 288, 512
+    W = synth.weights(N, K, seed=group + 11, heavy=True)
+    am = oracle.act_absmax(synth.activations(512, K, seed=K).astype(np.float16))
+    s = oracle.smooth_scales(oracle.weight_absmax(W), am, 0.5)
+    nf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    q = sq.quantize_pack_groupwise(_t(W), _t(s), group=group, nonfinite=nf, zeros_u4=True)
+    assert q.zeros.shape == (K // group, N // 2) and q.zeros.dtype == torch.uint8
+    _check_quant(W, s, q, nonfinite=nf, group=group)
+    E = synth.edge_groups(group, seed=group)
+    pad = (-E.shape[0]) % 32
+    We = np.concatenate([E, synth.weights(pad, group, seed=6)]).astype(np.float16)
+    We = np.tile(We, (1, 128 // group))
+    We[3, 0] = np.inf                                            # a non-finite group: Z = 0
+    nf.zero_()
+    qe = sq.quantize_pack_groupwise(_t(We), group=group, nonfinite=nf, zeros_u4=True)
+    _check_quant(We, None, qe, nonfinite=nf, group=group)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("group", [128, 32])
+@pytest.mark.parametrize("path,M", [(sq.SQ_PATH_DECODE, 1), (sq.SQ_PATH_DECODE, 4), (sq.SQ_PATH_DECODE, 16),
+                                    (sq.SQ_PATH_PREFILL, 17), (sq.SQ_PATH_PREFILL, 64), (sq.SQ_PATH_PREFILL, 300)])
+@pytest.mark.parametrize("N,K", [(288, 1152), (2048, 4096)])
+def test_gemm_zeros_u4_parity(path, M, N, K, group, dtype):
+    """W4A16 GEMM with packed u4 zero points through both paths (ragged 32/64/128-row blocks,
+    ragged stages, stream-K) against the oracle element by element, and BIT-identical to the
+    same GEMM with fp16 zero points (Z is the same integer either way)."""
+    c = _gemm_case(M, N, K, dtype, path, seed=M + group, group=group, zeros_u4=True)
+    c.check(dtype)
+    c16 = _gemm_case(M, N, K, dtype, path, seed=M + group, group=group, zeros_u4=False)
+    assert torch.equal(c.y, c16.y)
