@@ -45,12 +45,13 @@ struct Fmt<false> {
   static constexpr uint32_t kExpMask = 0x7C00u;
   __device__ static float to_f(uint16_t b) { return __half2float(__ushort_as_half(b)); }
   __device__ static uint16_t from_f_rn(float f) { return __half_as_ushort(__float2half_rn(f)); }
+  // NaN-propagating: a NaN anywhere in the group reaches the reduced min and max
   __device__ static uint32_t min2(uint32_t a, uint32_t b) {
-    __half2 r = __hmin2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    __half2 r = __hmin2_nan(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
     return *reinterpret_cast<uint32_t*>(&r);
   }
   __device__ static uint32_t max2(uint32_t a, uint32_t b) {
-    __half2 r = __hmax2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    __half2 r = __hmax2_nan(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
     return *reinterpret_cast<uint32_t*>(&r);
   }
 };
@@ -62,13 +63,13 @@ struct Fmt<true> {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
   }
   __device__ static uint32_t min2(uint32_t a, uint32_t b) {
-    __nv_bfloat162 r = __hmin2(*reinterpret_cast<__nv_bfloat162*>(&a),
-                               *reinterpret_cast<__nv_bfloat162*>(&b));
+    __nv_bfloat162 r = __hmin2_nan(*reinterpret_cast<__nv_bfloat162*>(&a),
+                                   *reinterpret_cast<__nv_bfloat162*>(&b));
     return *reinterpret_cast<uint32_t*>(&r);
   }
   __device__ static uint32_t max2(uint32_t a, uint32_t b) {
-    __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a),
-                               *reinterpret_cast<__nv_bfloat162*>(&b));
+    __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&a),
+                                   *reinterpret_cast<__nv_bfloat162*>(&b));
     return *reinterpret_cast<uint32_t*>(&r);
   }
 };
@@ -127,20 +128,20 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
         w[2 * q + 1] = lo1 | (hi1 << 16);
       }
     }
-    // non-finite detection (abs bits >= exponent mask) and min / max
-    uint32_t amax = 0, mn = w[0], mx = w[0];
+    // min / max with NaN propagation; a NaN or ±Inf in the group then shows in mn or mx,
+    // so the non-finite test (abs bits >= exponent mask) runs once per group on them
+    uint32_t mn = w[0], mx = w[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      amax = __vmaxu2(amax, w[i] & 0x7FFF7FFFu);
+    for (int i = 1; i < 8; ++i) {
       mn = Fmt<kBF16>::min2(mn, w[i]);
       mx = Fmt<kBF16>::max2(mx, w[i]);
     }
 #pragma unroll
     for (int o = 1; o < kLanesPerGroup; o <<= 1) {
-      amax = __vmaxu2(amax, __shfl_xor_sync(0xffffffffu, amax, o));
       mn = Fmt<kBF16>::min2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       mx = Fmt<kBF16>::max2(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
+    const uint32_t amax = __vmaxu2(mn & 0x7FFF7FFFu, mx & 0x7FFF7FFFu);
     bool nf = ((amax & 0xFFFFu) >= Fmt<kBF16>::kExpMask) || ((amax >> 16) >= Fmt<kBF16>::kExpMask);
     const float lo = fminf(Fmt<kBF16>::to_f(mn & 0xFFFFu), Fmt<kBF16>::to_f(mn >> 16));
     const float hi = fmaxf(Fmt<kBF16>::to_f(mx & 0xFFFFu), Fmt<kBF16>::to_f(mx >> 16));
@@ -181,18 +182,26 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
         // 2^-12 cannot cross one.  |x| >= 16 is clamped below whichever way it rounds, and
         // |x| < 2^15 - 16 always (Δ >= (r / 15)(1 - 2^-10) and r >= |v| 2^-11), so the
         // integer c + Z fits the signed 16-bit lanes of the clamp.
-        const int zoff = (int)z - 0x4B400000;  // + Z, - the bits of 1.5 * 2^23
+        // The magic constant carries + Z: RN(v * inv' + 1.5 * 2^23 + Z) is 1.5 * 2^23 + Z + c
+        // (no exact ties remain, see above), whose float bits are 0x4B400000 + (Z + c), so the
+        // low 16 bits ARE the signed code Z + c (|Z + c| < 2^15): no subtraction needed.
+        const float cz = 12582912.0f + z;
+        uint32_t bytes[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {  // element pair (2q, 2q + 1) = the two halves of w[q]
           const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-          const int c0 = __float_as_int(__fmaf_rn(f.x, inv, 12582912.0f)) + zoff;
-          const int c1 = __float_as_int(__fmaf_rn(f.y, inv, 12582912.0f)) + zoff;
-          uint32_t cc = __byte_perm((uint32_t)c0, (uint32_t)c1, 0x5410);  // (c0, c1) as s16x2
+          const uint32_t b0 = __float_as_uint(__fmaf_rn(f.x, inv, cz));
+          const uint32_t b1 = __float_as_uint(__fmaf_rn(f.y, inv, cz));
+          uint32_t cc = __byte_perm(b0, b1, 0x5410);  // (Z + c0, Z + c1) as s16x2
           asm("max.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0u));
           asm("min.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0x000F000Fu));
-          const uint32_t byte = (cc & 0xFu) | ((cc >> 12) & 0xF0u);    // low nibble = even k
-          packed[q >> 2] += byte << (8 * (q & 3));
+          bytes[q] = (cc | (cc >> 12)) & 0xFFu;  // low nibble = even k
         }
+        // gather the eight bytes: two PRMTs per pair of bytes, one per word
+        packed[0] = __byte_perm(__byte_perm(bytes[0], bytes[1], 0x0040), __byte_perm(bytes[2], bytes[3], 0x0040),
+                                0x5410);
+        packed[1] = __byte_perm(__byte_perm(bytes[4], bytes[5], 0x0040), __byte_perm(bytes[6], bytes[7], 0x0040),
+                                0x5410);
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
