@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-gates", action="store_true", help="skip the per-shape gate chains (ncu launch lists)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-u4", action="store_true", help="skip the packed-u4-zero-point decode chains")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--backend", default="nccl", help="collective backend (gloo: test the TP path "
                     "with several ranks on one GPU, together with --one-device --no-graph)")
@@ -592,6 +593,27 @@ def main():
                                    "byte_weighted_mean_frac": sum(f * b_ for f, b_ in fr) / sum(b_ for _, b_ in fr),
                                    "how": "per 34B linear x M in the step: 48-launch CUDA-graph chain of the "
                                           "shape's layers, algorithmic bytes / event time per launch"}
+
+    # ---------------- N3: the same per-shape decode chains with the packed u4
+    # zero points (SQ_ZEROS_U4, quantized into the u4 layout by the product quantizer): 1.5 B
+    # less per group row (1.1 % of the decode bytes at g = 128)
+    if world == 1 and not a.skip_gates and not a.skip_u4:
+        st_u4 = stack.build_stack(model, a.layers, 0, 1, dev, zeros_u4=True)
+        torch.cuda.synchronize()
+        gz = {}
+        for si, sh in enumerate(st_u4.shards):
+            rows = {}
+            for b in bufs:
+                t_l = chain_time(st_u4, si, b, max(3, a.steps // 3), not a.no_graph)
+                bl = tp.decode_bytes(b.M, sh.K, sh.N, zeros_u4=True)
+                t16 = gates["decode"][f"{sh.name} {sh.K}x{sh.N}"][str(b.M)]["us_per_launch"] * 1e-6
+                rows[str(b.M)] = {"us_per_launch": t_l * 1e6, "GB/s": bl / t_l / 1e9,
+                                  "frac": bl / t_l / 1e9 / hbm_peak, "bytes": bl,
+                                  "time_vs_fp16_zeros": t_l / t16}
+            gz[f"{sh.name} {sh.K}x{sh.N}"] = rows
+        gates["decode_zeros_u4"] = gz
+        del st_u4
+        torch.cuda.empty_cache()
 
     # ---------------- BASELINE.json configs[1]: Code Llama-7B decode shapes on 1 GPU
     cfg7 = None

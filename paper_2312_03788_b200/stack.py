@@ -58,14 +58,15 @@ def synth_act_max(K: int, seed: int, device) -> torch.Tensor:
 
 def build_stack(model: ModelShape = CODELLAMA_34B, layers: int | None = None, rank: int = 0,
                 world: int = 1, device="cuda", seed: int = 1234, smooth: bool = True,
-                group=None) -> LinearStack:
+                group=None, zeros_u4: bool = False) -> LinearStack:
     """Quantize `layers` decoder layers' linears for this rank (setup, not timed).  Each
     rank draws only its own shard.  Eq. 6's weight maxima are those of the FULL weight: a
     column-parallel shard holds some output rows of every input channel, so the ranks
     all-reduce their shard's column maxima with MAX before computing s (every rank folds
     the same s, as a real tensor-parallel deployment of Eq. 5/6 would); a row-parallel
     shard holds whole input channels, so its maxima are already complete.  The returned
-    weights are resident and final, so their GEMMs run with SQ_GEMM_WEIGHTS_STATIC."""
+    weights are resident and final, so their GEMMs run with SQ_GEMM_WEIGHTS_STATIC.
+    zeros_u4: the zero points in the packed u4 layout (SQ_ZEROS_U4)."""
     import torch.distributed as dist
 
     L = model.layers if layers is None else layers
@@ -82,7 +83,7 @@ def build_stack(model: ModelShape = CODELLAMA_34B, layers: int | None = None, ra
                 if group is not None and world > 1 and sh.kind == "col":
                     dist.all_reduce(w_max, op=dist.ReduceOp.MAX, group=group)
                 s = sq.smooth_scales_wmax(w_max, am, 0.5)
-            row.append(Linear(sh, sq.quantize_pack_groupwise(W, s)))
+            row.append(Linear(sh, sq.quantize_pack_groupwise(W, s, zeros_u4=zeros_u4)))
             del W
         st.layers.append(row)
     torch.cuda.synchronize(device)  # the quantize kernels are done: the weights are final

@@ -104,15 +104,15 @@ def full_shapes(m: ModelShape) -> list[tuple[str, int, int]]:
             ("gate_up", m.hidden, 2 * m.mlp), ("down_proj", m.mlp, m.hidden)]
 
 
-def w4_bytes(K: int, N: int, group: int = GROUP) -> int:
-    """Bytes of the W4 g128 layout: codes + fp16 Δ + fp16 Z."""
-    return K * N // 2 + 4 * N * (K // group)
+def w4_bytes(K: int, N: int, group: int = GROUP, zeros_u4: bool = False) -> int:
+    """Bytes of the W4 layout: codes + fp16 Δ + fp16 Z (or packed u4 Z, SQ_ZEROS_U4)."""
+    return K * N // 2 + 2 * N * (K // group) + (N * (K // group) // 2 if zeros_u4 else 2 * N * (K // group))
 
 
-def decode_bytes(M: int, K: int, N: int, group: int = GROUP) -> int:
+def decode_bytes(M: int, K: int, N: int, group: int = GROUP, zeros_u4: bool = False) -> int:
     """Algorithmic HBM bytes of one W4A16 GEMM:
-    K·N/2 + 4·N·K/g + 2·M·K + 2·M·N."""
-    return w4_bytes(K, N, group) + 2 * M * K + 2 * M * N
+    K·N/2 + 4·N·K/g + 2·M·K + 2·M·N (u4 zeros: 2.5·N·K/g for Δ and Z)."""
+    return w4_bytes(K, N, group, zeros_u4) + 2 * M * K + 2 * M * N
 
 
 def gemm_flops(M: int, K: int, N: int) -> int:

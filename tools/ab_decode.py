@@ -66,6 +66,8 @@ def main():
     for name, (K, N) in shapes.items():
         wb = K * N // 2 + 4 * N * K // 128
         copies = max(2, (4 * l2) // wb + 1) if cold else (1 if os.environ.get("AB_WARM_L2") else 2)
+        if os.environ.get("AB_COPIES"):  # working-set probe: this many distinct weight copies
+            copies = int(os.environ["AB_COPIES"])
         W = (torch.randn(N, K, device=dev) * 0.02).half()
         q0 = sq.quantize_pack_groupwise(W)
         del W

@@ -19,19 +19,20 @@ def main():
     ap.add_argument("--K", type=int, default=8192)
     ap.add_argument("--N", type=int, default=22016)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--path", type=int, default=None, help="explicit SQ_PATH_* (3 = tcgen05 decode)")
+    ap.add_argument("--path", type=int, default=None, help="explicit SQ_PATH_*")
+    ap.add_argument("--zeros-u4", action="store_true", help="packed u4 zero points (SQ_ZEROS_U4)")
     a = ap.parse_args()
     dev = "cuda"
     W = (torch.randn(a.N, a.K, device=dev) * 0.02).half()
     s = torch.rand(a.K, device=dev) + 0.5
     if a.kind == "quant":
         for _ in range(a.reps):
-            sq.quantize_pack_groupwise(W, s)
+            sq.quantize_pack_groupwise(W, s, zeros_u4=a.zeros_u4)
     elif a.kind == "smooth":
         for _ in range(a.reps):
             sq.smooth_scales(W, s, 0.5)
     else:
-        q = sq.quantize_pack_groupwise(W, s)
+        q = sq.quantize_pack_groupwise(W, s, zeros_u4=a.zeros_u4)
         M = a.M or (16 if a.kind == "decode" else 2048)
         x = torch.randn(M, a.K, device=dev).half()
         y = torch.empty(M, a.N, device=dev, dtype=torch.half)

@@ -4,8 +4,9 @@
 
 C1 (BASELINE.json configs[0]: K = N = 512, M = 1) end to end, plus one ragged / tail shape per
 kernel: decode at M = 1 and 16 under both schedules (stream-K fixups, row blocks), prefill with
-stream-K and a ragged token tile, quantize with edge groups, the one-shot all-reduce and the
-fused GEMM + all-reduce (one rank).  Results are checked against
+stream-K and a ragged token tile, quantize with edge groups, the packed u4 zero-point layout
+(SQ_ZEROS_U4: quantizer, decode at M = 1 / 16, prefill, g = 128 and 32), the one-shot all-reduce
+and the fused GEMM + all-reduce (one rank).  Results are checked against
 the plain relations (no oracle needed here; the parity tests do that), so a sanitizer run also
 fails loudly on wrong output.
 """
@@ -60,6 +61,18 @@ def main():
     qp = sq.quantize_pack_groupwise(Wp)
     for M in (17, 300):
         sq.w4a16_gemm(torch.randn(M, 2048, device=DEV).half(), qp, path=sq.SQ_PATH_PREFILL)
+    # packed u4 zero points (N3): quantizer output, decode (both schedules' tails: N = 288 is a
+    # ragged 64-row block) and prefill, g = 128 and 32; results equal the fp16-Z GEMM bit for bit
+    Wu = torch.from_numpy(synth.weights(288, 1152, seed=11)).to(DEV)
+    for g in (128, 32):
+        qz = sq.quantize_pack_groupwise(Wu, group=g, zeros_u4=True)
+        qf = sq.quantize_pack_groupwise(Wu, group=g)
+        for M, path in ((1, sq.SQ_PATH_DECODE), (16, sq.SQ_PATH_DECODE), (40, sq.SQ_PATH_PREFILL)):
+            xu = torch.randn(M, 1152, device=DEV).half()
+            a = sq.w4a16_gemm(xu, qz, path=path)
+            b = sq.w4a16_gemm(xu, qf, path=path)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), (g, M)
     # one-shot all-reduce and fused GEMM + all-reduce.  One rank (the sanitizer may serialize
     # concurrent kernels, and two simulated ranks must be co-resident); push, flag, wait and
     # reduce all run with world = 1 too.
