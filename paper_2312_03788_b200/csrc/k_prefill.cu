@@ -471,17 +471,17 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
     const int sw = (row >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk c of the row sits at c ^ ((row >> 1) & 3)
     uint32_t dph = 0;
     int j = 0;  // code-stage counter over the CTA's whole sequence (ring slot j % NSC, phase (j / NSC) & 1)
+    // APS == 1: this set's next stage jn = ch, ch + R, ... and its code / A ring slots and phases
+    static_assert(R < NSC && R < NSA, "one wrap per step");
+    int jn = ch, cs_n = ch % NSC, sl_n = ch % NSA;
+    uint32_t cph_n = (uint32_t)((ch / NSC) & 1), aph_n = (uint32_t)((ch / NSA) & 1);
     for (PSched sc(blockIdx.x, gridDim.x, G, num_tiles, sk, cta_q, cta_r); sc.valid(); sc.next()) {
       const int tile = sc.tile;
       const int n0 = (tile / m_tiles) * BM;
       const int m0 = (tile % m_tiles) * BT;
-      for (int g = sc.g0; g < sc.g1; ++g, ++j) {
-        // this set's A stage of the code stage: t = ch (APS = R), or the whole stage (APS = 1)
-        if (APS == 1 && j % R != ch) continue;
-        const int t = APS == 1 ? 0 : ch;
-        const int i = j * APS + t;  // A-stage counter
-        const int cs = j % NSC;
-        mbar_wait(c_full(cs), (j / NSC) & 1);
+      // convert one A stage: code-ring slot cs (phase cph), A stage t of it, TMEM A slot (phase aph)
+      auto convert = [&](int cs, uint32_t cph, int t, int slot, uint32_t aph) {
+        mbar_wait(c_full(cs), cph);
         const uint32_t crow = sbase + C::OFF_C + cs * C_STAGE_BYTES + row * (kGroup / 2);
         constexpr int NCH = KA / 32;  // 16-byte chunks of the A stage in the row
         uint32_t words[KA / 8];
@@ -516,8 +516,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
           df[h] = __half2float(__ushort_as_half(sbits[h]));
           sat |= !kBF16 && df[h] > 4366.0f;
         }
-        const int slot = i % NSA;
-        mbar_wait(a_empty(slot), ((i / NSA) & 1) ^ 1);
+        mbar_wait(a_empty(slot), aph ^ 1);
         tc_fence_after();
         // dequantize and store 64 k (32 TMEM columns) at a time
 #pragma unroll
@@ -542,7 +541,25 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full(slot));
+      };
+      const int jend = j + (sc.g1 - sc.g0);
+      if constexpr (APS == 1) {
+        // whole code stages, this set's every R-th one: running ring indices, no per-stage
+        // division (the skip loop and its modulo were ~5 % of the kernel's instructions)
+        for (; jn < jend; jn += R) {
+          convert(cs_n, cph_n, 0, sl_n, aph_n);
+          cs_n += R;
+          if (cs_n >= NSC) { cs_n -= NSC; cph_n ^= 1u; }
+          sl_n += R;
+          if (sl_n >= NSA) { sl_n -= NSA; aph_n ^= 1u; }
+        }
+      } else {
+        for (int jj = j; jj < jend; ++jj) {
+          const int i = jj * APS + ch;  // A-stage counter
+          convert(jj % NSC, (jj / NSC) & 1, ch, i % NSA, (i / NSA) & 1);
+        }
       }
+      j = jend;
       // ---- epilogue: D[row][token] -> Y[m0 + token][n0 + row]
       pdl_wait();  // (returns at once after the first tile) Y may be read by the previous kernel
       mbar_wait(d_full, dph);
