@@ -47,7 +47,7 @@ constexpr int kCtasPerSm = 2;      // M >= 2 (and M = 1 outside the 3-CTA rule):
 // M = 1: three 74-KB CTAs per SM for 32-64 MB layers that two CTAs would stream-K (7B gate|up -12 %,
 // 34B qkv -1-2 %; profiles/decode_m1_ct3_ab_r01.jsonl)
 constexpr int kMaxCtasPerSm = 3;   // workspace partial slots are sized for the most CTAs a launch can have
-constexpr int kMaxBN = 64;         // row-block heights: 32 or 64
+constexpr int kMaxBN = 64;         // row-block heights: 32 or 64 (128 at M = 1, within the same partial slots)
 constexpr int kMinBN = 32;
 // try_wait suspend-time hint of the producer / epilogue waits (ns)
 constexpr uint32_t kIdleWaitNs = 100000;
@@ -81,6 +81,7 @@ struct Cfg {
   static constexpr int PARK_STRIDE = kParkCodes ? BN * 64 : XSLICE;
   static_assert(XR * BN * 4 <= PARK_STRIDE, "partial-sum slot must fit");
   static_assert(XR * BN >= 32, "epilogue lanes");
+  static_assert(XR * BN <= 16 * kMaxBN, "stream-K partial slot (16 x kMaxBN fp32) must hold a row block");
   static constexpr int OFF_BAR = NS * STAGE;  // full[NS], empty[NS], red_full[NS]
   static constexpr int SMEM = OFF_BAR + 3 * NS * 8;
   static constexpr int SMEM_ALLOC = SMEM + 1024;
@@ -848,6 +849,15 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     // Decide from N alone (K differs between row-parallel shards): stream-K, 64-row blocks.
     dp = false;
     bn = 64;
+  }
+  // M = 1 on layers of >= 48 MB of codes (stream-K, two CTAs per SM): 128-row blocks -- a
+  // stage then carries 32 KB of codes per barrier round and X fragment, and each consumer
+  // warp runs eight row tiles per stage; 4-6 % faster on the 34B gate|up, gate and down
+  // shapes (profiles/r02/decode_bn128_ab.jsonl), +-2 % at M = 4-8, so M = 1 only
+  if constexpr (XR == 1 && CT == 2) {
+    if (!dp && bn == 64 && ar.world == 0 && (double)N * K / 2 >= 48.0 * 1024 * 1024)
+      return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
+                                              grid_per_sm, st, why);
   }
   if (bn == 32)
     return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4, grid_per_sm,
