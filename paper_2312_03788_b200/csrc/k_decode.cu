@@ -850,12 +850,15 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     dp = false;
     bn = 64;
   }
-  // M = 1 on layers of >= 48 MB of codes (stream-K, two CTAs per SM): 128-row blocks -- a
-  // stage then carries 32 KB of codes per barrier round and X fragment, and each consumer
-  // warp runs eight row tiles per stage; 4-6 % faster on the 34B gate|up, gate and down
-  // shapes (profiles/r02/decode_bn128_ab.jsonl), +-2 % at M = 4-8, so M = 1 only
+  // M = 1 on layers of >= 48 MB of codes, or >= 32 MB with K >= 8192 (stream-K, two CTAs per
+  // SM): 128-row blocks -- a stage then carries 32 KB of codes per barrier round and X
+  // fragment, and each consumer warp runs eight row tiles per stage; 4-6 % faster on the 34B
+  // gate|up, gate, down and qkv shapes (profiles/r02/decode_bn128_ab.jsonl,
+  // decode_bn128_threshold_ab.jsonl), +-2 % at M = 4-8, so M = 1 only
   if constexpr (XR == 1 && CT == 2) {
-    if (!dp && bn == 64 && ar.world == 0 && (double)N * K / 2 >= 48.0 * 1024 * 1024)
+    const double codes = (double)N * K / 2;
+    if (!dp && bn == 64 && ar.world == 0 &&
+        (codes >= 48.0 * 1024 * 1024 || (codes >= 32.0 * 1024 * 1024 && K >= 8192)))
       return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
                                               grid_per_sm, st, why);
   }
@@ -920,8 +923,9 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
     // Not for the fused all-reduce (its row-block cut must not depend on the rank's K).
     const double codes = (double)N * K / 2;
     int rbn = 64;
+    // (K >= 8192 layers of this size take two CTAs per SM with 128-row blocks instead, launch_m)
     if (ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO && codes >= 32.0 * 1024 * 1024 &&
-        codes <= 64.0 * 1024 * 1024 && !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn))
+        codes < 48.0 * 1024 * 1024 && K < 8192 && !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn))
       return bf16 ? launch_m<1, true, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
                   : launch_m<1, false, 1, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
     return bf16 ? launch_m<1, true, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
