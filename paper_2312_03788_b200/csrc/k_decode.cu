@@ -931,6 +931,15 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
     return bf16 ? launch_m<1, true, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
                 : launch_m<1, false, 1, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   }
+  // M = 2-4 on whole-row-block layers and K < 8192 layers: stage only four activation rows
+  // (4-KB X slices, a deeper ring): 34B o_proj -2 %, the 7B shapes -5 %; the big stream-K
+  // 34B layers stay on eight rows (+1-2 % with four; profiles/r02/decode_xr4_ab.jsonl)
+  int rbn4 = 64;
+  const bool xr4 = M <= 4 && ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO &&
+                   (K < 8192 || auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn4));
+  if (xr4)
+    return bf16 ? launch_m<1, true, 4, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+                : launch_m<1, false, 4, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   if (M <= 8)
     return bf16 ? launch_m<1, true, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
                 : launch_m<1, false, 8, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
