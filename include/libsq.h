@@ -24,7 +24,7 @@
  *  - scales[G][N] and zeros[G][N] are fp16 bit patterns (uint16), group-major:
  *    scales[gi][n] is Delta of the group (n, k in [gi*group, (gi+1)*group)).
  *    zeros hold integers 0..15 stored as fp16.  With SQ_ZEROS_U4 (SURVEY.md §8(f) N3,
- *    SPEC.md:185-186 "Z: u4") zeros are instead PACKED uint8[G][N/2]: Z of channel n is
+ *    SPEC.md:185 "Z stored as unsigned 4-bit") zeros are instead PACKED uint8[G][N/2]: Z of channel n is
  *    the LOW nibble of byte zeros[gi][n/2] when n is even, the HIGH nibble when n is
  *    odd (the nibble order of the codes, along n; oracle/sq_oracle.py pack_zeros_u4).
  *    The packed layout needs N % 32 == 0 (16-byte rows for TMA), else SQ_ERR_ALIGN.
