@@ -122,3 +122,25 @@ def test_fullsize_bf16_activations_and_large_m():
     y_ref = X2.cpu().numpy()[toks].astype(np.float64) @ W_hat2.T
     y = Y2.cpu().numpy()[np.ix_(toks, rows2)].astype(np.float64)
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= 1e-3
+
+
+@pytest.mark.parametrize("name", ["qkv", "o_proj", "gate_up", "down", "7b_gate_up", "7b_o_proj"])
+def test_fullsize_decode_vs_prefill_all_rows(name):
+    """EVERY output of the decode kernel at M = 1, 3 and 16 (the 128-row-block, four-row and
+    sixteen-row configurations of the full-size shapes) against the independently written
+    prefill kernel on the same weights: the two paths round differently (exact (q - Z) with
+    fp32 Δ vs Ŵ = RN((q - Z) Δ)), so they agree to the fp16 bound, and a wrong
+    row block, stage or fixup -- which sampled rows could miss -- is an O(1) difference."""
+    K, N = SHAPES[name]
+    W = stack.synth_weight(N, K, 200 + list(SHAPES).index(name), DEV)
+    q = sq.quantize_pack_groupwise(W).mark_static()
+    g = torch.Generator(device=DEV).manual_seed(201)
+    for M in (1, 3, 16):
+        X = torch.randn(M, K, generator=g, device=DEV).half()
+        yd = sq.w4a16_gemm(X, q, path=sq.SQ_PATH_DECODE).float()
+        yp = sq.w4a16_gemm(X, q, path=sq.SQ_PATH_PREFILL).float()
+        torch.cuda.synchronize()
+        rel = ((yd - yp).norm() / yp.norm()).item()
+        assert rel <= 2e-3, (name, M, rel)
+        worst = ((yd - yp).abs() / (yp.abs() + 1e-2 * yp.abs().max())).max().item()
+        assert worst <= 0.05, (name, M, worst)
