@@ -116,6 +116,8 @@ def main():
              gemm_b(2048, 8192, 22016)),
             ("prefill_m32", "prof_prefill_m32_gateup.ncu-rep", "prefill GEMM, M=32, K=8192, N=44032 (mid-M)",
              gemm_b(32, 8192, 44032)),
+            ("decode_m1_qkv", "prof_decode_m1_qkv_r02c.ncu-rep", "decode GEMM, M=1, K=8192, N=10240 (34B qkv)",
+             gemm_b(1, 8192, 10240)),
             ("decode_m1_u4", "prof_decode_m1_gateup_u4.ncu-rep",
              "decode GEMM, M=1, K=8192, N=44032, packed u4 zero points (SQ_ZEROS_U4)",
              gemm_b(1, 8192, 44032) - 3 * 44032 * 64 // 2),
