@@ -51,12 +51,15 @@ constexpr int SZ_BYTES = (kGroup / 32) * BM * 2;  // Δ (or Z) rows of a stage: 
 //    ~850-1050 cycles converting a stage and ~650 more in barrier checks and hand-offs
 //    (profiles/r02/prefill_midm_trace.txt); whole-group stages halve the hand-offs per weight
 //    and the third set fills the sub-partition while another waits.
-template <int kBT>
+template <int kBT, int kR = (kBT == kBTMax ? 2 : 3)>
 struct PCfg {
   static constexpr int BT = kBT;
   static constexpr int KA = kBT == kBTMax ? 64 : 128;  // k per A stage and per X stage
   static constexpr int APS = kGroup / KA;               // A stages per code stage
-  static constexpr int R = kBT == kBTMax ? 2 : 3;       // dequant warp sets (4 or 5: no faster)
+  // dequant warp sets: 3 at M <= 48 and 65-128; 4 at M = 49-64, where the 64-row X stages
+  // make the MMA side slower and a fourth set keeps more A stages converted (5-9 % on the
+  // 34B shapes but gate|up, profiles/r02/prefill_four_sets_ab.jsonl; 2-4 % slower at M <= 32)
+  static constexpr int R = kR;
   static constexpr int DQW = 4 * R;                     // dequant / epilogue warps
   static constexpr int THREADS = (kDequantWarp0 + DQW) * 32;
   static constexpr int X_SUB_BYTES = BT * 128;          // one 64-k SWIZZLE_128B box of BT rows
@@ -334,14 +337,14 @@ struct PSched {
   }
 };
 
-template <bool kBF16, int GS, int kBT>
-__global__ void __launch_bounds__(PCfg<kBT>::THREADS, 1)
+template <bool kBF16, int GS, int kBT, int kR>
+__global__ void __launch_bounds__(PCfg<kBT, kR>::THREADS, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_z,
                uint16_t* __restrict__ Y, int M, int N, int K, int early_weights, int x_bytes,
                int sk, int cta_q, int cta_r, float* __restrict__ partials, int* __restrict__ counters,
                int zu4) {
-  using C = PCfg<kBT>;
+  using C = PCfg<kBT, kR>;
   constexpr int BT = C::BT, KA = C::KA, APS = C::APS, R = C::R, DQW = C::DQW;
   constexpr int NSX = C::NSX, NSC = C::NSC, NSA = C::NSA;
   constexpr int SUBS = kGroup / GS;  // Δ/Z rows per stage
@@ -703,17 +706,17 @@ size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 }
 
 namespace {
-template <bool kBF16, int kBT>
+template <bool kBF16, int kBT, int kR>
 auto pick_kernel(int group) {
-  return group == 32 ? prefill_kernel<kBF16, 32, kBT> : group == 64 ? prefill_kernel<kBF16, 64, kBT>
-                                                                    : prefill_kernel<kBF16, 128, kBT>;
+  return group == 32 ? prefill_kernel<kBF16, 32, kBT, kR>
+                     : group == 64 ? prefill_kernel<kBF16, 64, kBT, kR> : prefill_kernel<kBF16, 128, kBT, kR>;
 }
 
-template <int kBT>
+template <int kBT, int kR = (kBT == kBTMax ? 2 : 3)>
 cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint16_t* scales, const void* zeros,
                       void* Y, int M, int N, int K, int group, void* ws, bool weights_static, bool zu4,
                       cudaStream_t st, const char** why) {
-  using C = PCfg<kBT>;
+  using C = PCfg<kBT, kR>;
   alignas(64) CUtensorMap tm_x, tm_w, tm_s, tm_z;
   const int G = (int)prefill_stages(M, K);
   // X box: 64 k (one SWIZZLE_128B row) of only as many token rows as the problem has (OOB
@@ -742,7 +745,7 @@ cudaError_t launch_bt(const void* X, int x_dtype, const uint8_t* Wq, const uint1
   const int cta_q = units / grid, cta_r = units % grid;
   float* partials = reinterpret_cast<float*>(ws);
   int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ws_partials_bytes());
-  auto kern = x_dtype == SQ_BF16 ? pick_kernel<true, kBT>(group) : pick_kernel<false, kBT>(group);
+  auto kern = x_dtype == SQ_BF16 ? pick_kernel<true, kBT, kR>(group) : pick_kernel<false, kBT, kR>(group);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_ALLOC);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -768,6 +771,8 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
                            bool weights_static, bool zu4, cudaStream_t st, const char** why) {
   switch (prefill_bt(M)) {
     case 64:
+      if (M > 48)  // four dequant warp sets at M = 49-64 (PCfg)
+        return launch_bt<64, 4>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
       return launch_bt<64>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
     case 128:
       return launch_bt<128>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);

@@ -450,3 +450,12 @@ def test_gemm_zeros_u4_parity(path, M, N, K, group, dtype):
     c.check(dtype)
     c16 = _gemm_case(M, N, K, dtype, path, seed=M + group, group=group, zeros_u4=False)
     assert torch.equal(c.y, c16.y)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("M", [48, 49, 57, 64])
+@pytest.mark.parametrize("N,K", [(392, 1152), (1024, 2048)])
+def test_gemm_prefill_warp_set_boundary(M, N, K, dtype):
+    """Prefill at the 48 | 49 boundary between the three- and four-warp-set configurations of
+    the 64-token tile (ragged N, ragged stream-K), against the oracle element by element."""
+    _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M + 7).check(dtype)
