@@ -56,9 +56,10 @@ struct PCfg {
   static constexpr int BT = kBT;
   static constexpr int KA = kBT == kBTMax ? 64 : 128;  // k per A stage and per X stage
   static constexpr int APS = kGroup / KA;               // A stages per code stage
-  // dequant warp sets: 3 at M <= 48 and 65-128; 4 at M = 49-64, where the 64-row X stages
-  // make the MMA side slower and a fourth set keeps more A stages converted (5-9 % on the
-  // 34B shapes but gate|up, profiles/r02/prefill_four_sets_ab.jsonl; 2-4 % slower at M <= 32)
+  // dequant warp sets: 4 when the token tile is more than three quarters full (M = 49-64 at
+  // BT = 64, 97-128 at BT = 128) -- the wider MMAs and X stages slow the MMA side and a fourth
+  // set keeps more A stages converted (3-10 % on the 34B shapes but gate|up, unchanged) --
+  // else 3 (a fourth set costs 2-4 % there); profiles/r02/prefill_four_sets_ab.jsonl
   static constexpr int R = kR;
   static constexpr int DQW = 4 * R;                     // dequant / epilogue warps
   static constexpr int THREADS = (kDequantWarp0 + DQW) * 32;
@@ -771,10 +772,12 @@ cudaError_t launch_prefill(const void* X, int x_dtype, const uint8_t* Wq, const 
                            bool weights_static, bool zu4, cudaStream_t st, const char** why) {
   switch (prefill_bt(M)) {
     case 64:
-      if (M > 48)  // four dequant warp sets at M = 49-64 (PCfg)
+      if (M > 48)  // four dequant warp sets when the 64-token tile is > 3/4 full (PCfg)
         return launch_bt<64, 4>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
       return launch_bt<64>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
     case 128:
+      if (M > 96)  // four dequant warp sets when the 128-token tile is > 3/4 full (PCfg)
+        return launch_bt<128, 4>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
       return launch_bt<128>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);
     default:
       return launch_bt<kBTMax>(X, x_dtype, Wq, scales, zeros, Y, M, N, K, group, ws, weights_static, zu4, st, why);

@@ -453,9 +453,10 @@ def test_gemm_zeros_u4_parity(path, M, N, K, group, dtype):
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("M", [48, 49, 57, 64])
+@pytest.mark.parametrize("M", [48, 49, 57, 64, 96, 97, 113, 128])
 @pytest.mark.parametrize("N,K", [(392, 1152), (1024, 2048)])
 def test_gemm_prefill_warp_set_boundary(M, N, K, dtype):
-    """Prefill at the 48 | 49 boundary between the three- and four-warp-set configurations of
-    the 64-token tile (ragged N, ragged stream-K), against the oracle element by element."""
+    """Prefill at the 48 | 49 and 96 | 97 boundaries between the three- and four-warp-set
+    configurations of the 64- and 128-token tiles (ragged N, ragged stream-K), against the
+    oracle element by element."""
     _gemm_case(M, N, K, dtype, sq.SQ_PATH_PREFILL, seed=M + 7).check(dtype)
