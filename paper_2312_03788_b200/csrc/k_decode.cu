@@ -44,8 +44,9 @@ constexpr int kGroup = 128;
 constexpr int GPS = 4;             // groups per stage (unit)
 constexpr int kConsumerWarps = 4;  // one per group of a stage; warp roles: consumers 0..3, TMA producer 4, epilogue 5
 constexpr int kCtasPerSm = 2;      // M >= 2 (and M = 1 outside the 3-CTA rule): two ~112-KB CTAs per SM
-// M = 1: three 74-KB CTAs per SM for 32-64 MB layers that two CTAs would stream-K (7B gate|up -12 %,
-// 34B qkv -1-2 %; profiles/decode_m1_ct3_ab_r01.jsonl)
+// M = 1: three 74-KB CTAs per SM for 32-48 MB layers with K < 8192 that two CTAs would stream-K
+// (7B gate|up -12 %; profiles/decode_m1_ct3_ab_r01.jsonl); larger / longer-K layers take two CTAs
+// with 128-row blocks (launch_m)
 constexpr int kMaxCtasPerSm = 3;   // workspace partial slots are sized for the most CTAs a launch can have
 constexpr int kMaxBN = 64;         // row-block heights: 32 or 64 (128 at M = 1, within the same partial slots)
 constexpr int kMinBN = 32;
@@ -917,10 +918,10 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   if (group == 32)
     return launch_small_group<32>(X, bf16, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   if (M == 1) {  // batch-1 decode: stage one activation row, smaller stages
-    // three 74-KB CTAs per SM for mid-sized layers (32-64 MB of codes) that two CTAs per SM
-    // would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
-    // measured -12 % on 7B gate|up, -2 % on 34B qkv (profiles/decode_m1_ct3_ab_r01.jsonl).
-    // Not for the fused all-reduce (its row-block cut must not depend on the rank's K).
+    // three 74-KB CTAs per SM for mid-sized layers (32-48 MB of codes, K < 8192) that two CTAs
+    // per SM would stream-K: more CTAs in flight (or a one-wave row-block split at 444 slots);
+    // measured -12 % on 7B gate|up (profiles/decode_m1_ct3_ab_r01.jsonl).  Not for the fused
+    // all-reduce (its row-block cut must not depend on the rank's K).
     const double codes = (double)N * K / 2;
     int rbn = 64;
     // (K >= 8192 layers of this size take two CTAs per SM with 128-row blocks instead, launch_m)
