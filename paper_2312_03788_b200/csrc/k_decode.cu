@@ -938,6 +938,14 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   int rbn4 = 64;
   const bool xr4 = M <= 4 && ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO &&
                    (K < 8192 || auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn4));
+  // ... and, like M = 1, three CTAs per SM on the 32-48 MB, K < 8192 stream-K layers (7B gate|up
+  // -10 % at M = 2-4; every other shape slower, profiles/r02/decode_ct3_m4_ab.jsonl)
+  int rbn3 = 64;
+  const double codes4 = (double)N * K / 2;
+  if (xr4 && codes4 >= 32.0 * 1024 * 1024 && codes4 < 48.0 * 1024 * 1024 && K < 8192 &&
+      !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn3))
+    return bf16 ? launch_m<1, true, 4, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
+                : launch_m<1, false, 4, 3>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
   if (xr4)
     return bf16 ? launch_m<1, true, 4, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why)
                 : launch_m<1, false, 4, kCtasPerSm>(X, Wq, scales, zeros, Y, M, N, K, ws, ar, weights_static, zu4, st, why);
