@@ -851,12 +851,13 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     dp = false;
     bn = 64;
   }
-  // M = 1 on layers of >= 48 MB of codes, or >= 32 MB with K >= 8192 (stream-K, two CTAs per
-  // SM): 128-row blocks -- a stage then carries 32 KB of codes per barrier round and X
-  // fragment, and each consumer warp runs eight row tiles per stage; 4-6 % faster on the 34B
-  // gate|up, gate, down and qkv shapes (profiles/r02/decode_bn128_ab.jsonl,
-  // decode_bn128_threshold_ab.jsonl), +-2 % at M = 4-8, so M = 1 only
-  if constexpr (XR == 1 && CT == 2) {
+  // M = 1-4 on layers of >= 48 MB of codes, or >= 32 MB with K >= 8192 (stream-K, two CTAs
+  // per SM): 128-row blocks -- a stage then carries 32 KB of codes per barrier round and X
+  // fragment, and each consumer warp runs eight row tiles per stage; 4-6 % faster at M = 1 on
+  // the 34B gate|up, gate, down and qkv shapes (profiles/r02/decode_bn128_ab.jsonl,
+  // decode_bn128_threshold_ab.jsonl), 1-5 % at M = 2-4 with four staged activation rows
+  // (decode_bn128_m4_ab.jsonl); with eight rows the stages get too deep for the ring (M = 5-8)
+  if constexpr (XR <= 4 && CT == 2) {
     const double codes = (double)N * K / 2;
     if (!dp && bn == 64 && ar.world == 0 &&
         (codes >= 48.0 * 1024 * 1024 || (codes >= 32.0 * 1024 * 1024 && K >= 8192)))
@@ -936,8 +937,12 @@ cudaError_t launch_decode(const void* X, int x_dtype, const uint8_t* Wq, const u
   // (4-KB X slices, a deeper ring): 34B o_proj -2 %, the 7B shapes -5 %; the big stream-K
   // 34B layers stay on eight rows (+1-2 % with four; profiles/r02/decode_xr4_ab.jsonl)
   int rbn4 = 64;
-  const bool xr4 = M <= 4 && ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO &&
-                   (K < 8192 || auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn4));
+  // The large K >= 8192 stream-K layers (>= 32 MB) stage four rows too, in 128-row blocks (launch_m)
+  const bool big4 = M <= 4 && ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO &&
+                    K >= 8192 && !auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn4) &&
+                    (double)N * K / 2 >= 32.0 * 1024 * 1024;
+  const bool xr4 = big4 || (M <= 4 && ar.world == 0 && option(SQ_OPT_DECODE_SCHEDULE) == SQ_SCHED_AUTO &&
+                            (K < 8192 || auto_rowblock(N, K, num_sms() * kCtasPerSm, &rbn4)));
   // ... and, like M = 1, three CTAs per SM on the 32-48 MB, K < 8192 stream-K layers (7B gate|up
   // -10 % at M = 2-4; every other shape slower, profiles/r02/decode_ct3_m4_ab.jsonl)
   int rbn3 = 64;
