@@ -835,7 +835,10 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // stream-K row-block height: 32 rows for M = 9..16 on layers below 48 MB of codes (half
   // the cut row blocks' fixup work; measured -8..-13 % on the 7B shapes, +2 % on 34B qkv),
   // 64 otherwise (larger stages stream faster)
-  int bn = MT == 2 && (double)N * K / 2 < 48.0 * 1024 * 1024 ? 32 : 64;
+  // ... and at M = 2-8 on layers below 32 MB (7B down, 8192 x 4096: -8-9 %; +3-11 % at M = 1,
+  // profiles/r02/decode_bn32_small_ab.jsonl)
+  const double codes_m = (double)N * K / 2;
+  int bn = (MT == 2 && codes_m < 48.0 * 1024 * 1024) || (MT == 1 && XR > 1 && codes_m < 32.0 * 1024 * 1024) ? 32 : 64;
   if (sched == SQ_SCHED_ROWBLOCK) {
     bn = rowblock_utilization(N, 64, slots) >= rowblock_utilization(N, 32, slots) ? 64 : 32;
   } else if (sched == SQ_SCHED_AUTO) {
