@@ -47,7 +47,7 @@ def main():
     path, ms = 1, (1, 16)
     if args and args[0] == "--prefill":
         path, ms, args = 2, (2048,), args[1:]
-    if args and args[0].startswith("--path="):  # 1 decode (mma.sync), 2 prefill, 3 decode_tc
+    if args and args[0].startswith("--path="):  # SQ_PATH_*: 1 decode (mma.sync), 2 prefill (tcgen05)
         path, args = int(args[0][7:]), args[1:]
     if args and args[0].startswith("--ms="):
         ms, args = tuple(int(v) for v in args[0][5:].split(",")), args[1:]
