@@ -862,6 +862,12 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // (decode_bn128_m4_ab.jsonl); with eight rows the stages get too deep for the ring (M = 5-8)
   if constexpr (XR <= 4 && CT == 2) {
     const double codes = (double)N * K / 2;
+    // (96-row blocks for the 32-48 MB ones at M = 1: 34B qkv -5 % against 128, every larger
+    // layer +1.5-7 %; profiles/r02/decode_bn96_ab.jsonl)
+    if (XR == 1 && !dp && bn == 64 && ar.world == 0 && codes >= 32.0 * 1024 * 1024 &&
+        codes < 48.0 * 1024 * 1024 && K >= 8192)
+      return launch_t<MT, kBF16, 96, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
+                                             grid_per_sm, st, why);
     if (!dp && bn == 64 && ar.world == 0 &&
         (codes >= 48.0 * 1024 * 1024 || (codes >= 32.0 * 1024 * 1024 && K >= 8192)))
       return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
