@@ -873,6 +873,14 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
       return launch_t<MT, kBF16, 128, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
                                               grid_per_sm, st, why);
   }
+  // M = 9-16, stream-K, 32-128 MB layers with 8192 <= K < 16384 (34B qkv, gate): 48-row
+  // blocks, between the 32-row (shallower work per stage) and 64-row (fewer, larger stages)
+  // choices: qkv -4-5 %, gate -3 %; gate|up (180 MB), down (K = 22016) and the 7B shapes do not
+  // gain (profiles/r02/decode_bn48_ab.jsonl)
+  if (MT == 2 && !dp && ar.world == 0 && codes_m >= 32.0 * 1024 * 1024 && codes_m < 128.0 * 1024 * 1024 &&
+      K >= 8192 && K < 16384)
+    return launch_t<MT, kBF16, 48, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
+                                           grid_per_sm, st, why);
   if (bn == 32)
     return launch_t<MT, kBF16, 32, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4, grid_per_sm,
                                            st, why);
