@@ -751,7 +751,8 @@ cudaError_t launch_t(const void* X, const uint8_t* Wq, const uint16_t* scales, c
     const uint64_t d[2] = {(uint64_t)N, (uint64_t)G * C::SUB};  // [K / GS][N]
     const uint64_t s[1] = {(uint64_t)N * 2};
     const uint32_t b[2] = {(uint32_t)BN, (uint32_t)(GPS * C::SUB)};
-    // packed u4 zeros: uint8[K / GS][N / 2], a box of BN / 2 bytes per zero row
+    // packed u4 zeros: uint8[K / GS][N / 2], a box of BN / 2 bytes per zero row (a multiple of
+    // 16 bytes: every row-block height the dispatch uses with u4 zeros -- 32, 64, 96, 128)
     const uint64_t dz[2] = {(uint64_t)N / 2, (uint64_t)G * C::SUB};
     const uint64_t sz[1] = {(uint64_t)N / 2};
     const uint32_t bz[2] = {(uint32_t)BN / 2, (uint32_t)(GPS * C::SUB)};
@@ -877,7 +878,9 @@ cudaError_t launch_m(const void* X, const uint8_t* Wq, const uint16_t* scales, c
   // blocks, between the 32-row (shallower work per stage) and 64-row (fewer, larger stages)
   // choices: qkv -4-5 %, gate -3 %; gate|up (180 MB), down (K = 22016) and the 7B shapes do not
   // gain (profiles/r02/decode_bn48_ab.jsonl)
-  if (MT == 2 && !dp && ar.world == 0 && codes_m >= 32.0 * 1024 * 1024 && codes_m < 128.0 * 1024 * 1024 &&
+  // (not with packed u4 zero points: a 48-row block's zero rows are 24 bytes, and a TMA box
+  // must span a multiple of 16 bytes)
+  if (MT == 2 && !dp && ar.world == 0 && !zu4 && codes_m >= 32.0 * 1024 * 1024 && codes_m < 128.0 * 1024 * 1024 &&
       K >= 8192 && K < 16384)
     return launch_t<MT, kBF16, 48, XR, CT>(X, Wq, scales, zeros, Y, M, N, K, ws, dp, ar, weights_static, zu4,
                                            grid_per_sm, st, why);

@@ -144,3 +144,24 @@ def test_fullsize_decode_vs_prefill_all_rows(name):
         assert rel <= 2e-3, (name, M, rel)
         worst = ((yd - yp).abs() / (yp.abs() + 1e-2 * yp.abs().max())).max().item()
         assert worst <= 0.05, (name, M, worst)
+
+
+@pytest.mark.parametrize("name", ["qkv", "o_proj", "gate_up", "down", "7b_gate_up", "7b_down"])
+def test_fullsize_zeros_u4_every_configuration(name):
+    """Packed u4 zero points (SQ_ZEROS_U4) through every decode configuration the full-size
+    shapes dispatch to (M = 1, 3, 9, 16: 32/48/64/96/128-row blocks, four/eight/sixteen staged
+    rows) and the prefill kernel (M = 40, 300): the launch must succeed (every TMA box of the
+    packed zero rows a multiple of 16 bytes) and agree with the fp16-Z result to fp32
+    summation order."""
+    K, N = SHAPES[name]
+    W = stack.synth_weight(N, K, 300 + list(SHAPES).index(name), DEV)
+    q16 = sq.quantize_pack_groupwise(W).mark_static()
+    q4 = sq.quantize_pack_groupwise(W, zeros_u4=True).mark_static()
+    g = torch.Generator(device=DEV).manual_seed(301)
+    for M in (1, 3, 9, 16, 40, 300):
+        X = torch.randn(M, K, generator=g, device=DEV).half()
+        y16 = sq.w4a16_gemm(X, q16).float()
+        y4 = sq.w4a16_gemm(X, q4).float()
+        torch.cuda.synchronize()
+        rel = ((y4 - y16).norm() / y16.norm()).item()
+        assert rel <= 1e-3, (name, M, rel)
