@@ -124,8 +124,9 @@ def test_fullsize_bf16_activations_and_large_m():
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= 1e-3
 
 
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("name", ["qkv", "o_proj", "gate_up", "down", "7b_gate_up", "7b_o_proj"])
-def test_fullsize_decode_vs_prefill_all_rows(name):
+def test_fullsize_decode_vs_prefill_all_rows(name, dtype):
     """EVERY output of the decode kernel at M = 1, 3 and 16 (the 128-row-block, four-row and
     sixteen-row configurations of the full-size shapes) against the independently written
     prefill kernel on the same weights: the two paths round differently (exact (q - Z) with
@@ -135,15 +136,16 @@ def test_fullsize_decode_vs_prefill_all_rows(name):
     W = stack.synth_weight(N, K, 200 + list(SHAPES).index(name), DEV)
     q = sq.quantize_pack_groupwise(W).mark_static()
     g = torch.Generator(device=DEV).manual_seed(201)
-    for M in (1, 3, 16):
-        X = torch.randn(M, K, generator=g, device=DEV).half()
+    tol = 2e-3 if dtype == torch.float16 else 1e-2  # bf16: 8-bit operands and outputs
+    for M in (1, 3, 9, 16):
+        X = torch.randn(M, K, generator=g, device=DEV).to(dtype)
         yd = sq.w4a16_gemm(X, q, path=sq.SQ_PATH_DECODE).float()
         yp = sq.w4a16_gemm(X, q, path=sq.SQ_PATH_PREFILL).float()
         torch.cuda.synchronize()
         rel = ((yd - yp).norm() / yp.norm()).item()
-        assert rel <= 2e-3, (name, M, rel)
+        assert rel <= tol, (name, M, rel)
         worst = ((yd - yp).abs() / (yp.abs() + 1e-2 * yp.abs().max())).max().item()
-        assert worst <= 0.05, (name, M, worst)
+        assert worst <= 25 * tol, (name, M, worst)
 
 
 @pytest.mark.parametrize("name", ["qkv", "o_proj", "gate_up", "down", "7b_gate_up", "7b_down"])
