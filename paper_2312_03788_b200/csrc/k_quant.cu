@@ -74,14 +74,25 @@ struct Fmt<true> {
   }
 };
 
-// RN_fmt(w * s) with a single rounding (round-to-odd in fp32, then RN).
+// w * s rounded to odd in fp32 (RZ product, sticky bit from the exact FMA residual): its
+// RN to fp16/bf16 is the single rounding RN_fmt(w * s) (24 >= 11 + 2 bits)
 template <bool kBF16>
-__device__ __forceinline__ uint16_t fold1(uint16_t wbits, float s) {
+__device__ __forceinline__ float fold_odd(uint16_t wbits, float s) {
   const float w = Fmt<kBF16>::to_f(wbits);
   float p = __fmul_rz(w, s);
   const float e = __fmaf_rn(w, s, -p);
   if (e != 0.0f) p = __uint_as_float(__float_as_uint(p) | 1u);
-  return Fmt<kBF16>::from_f_rn(p);
+  return p;
+}
+// two round-to-odd products -> RN pair in one packing conversion (F2FP)
+template <bool kBF16>
+__device__ __forceinline__ uint32_t pack_rn(float lo, float hi) {
+  if (kBF16) {
+    const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&b);
+  }
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 template <bool kBF16, int GS>
@@ -120,12 +131,9 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float4 sv = __ldg(sp + q);
-        const uint32_t lo0 = fold1<kBF16>(w[2 * q] & 0xFFFFu, sv.x);
-        const uint32_t hi0 = fold1<kBF16>(w[2 * q] >> 16, sv.y);
-        const uint32_t lo1 = fold1<kBF16>(w[2 * q + 1] & 0xFFFFu, sv.z);
-        const uint32_t hi1 = fold1<kBF16>(w[2 * q + 1] >> 16, sv.w);
-        w[2 * q] = lo0 | (hi0 << 16);
-        w[2 * q + 1] = lo1 | (hi1 << 16);
+        w[2 * q] = pack_rn<kBF16>(fold_odd<kBF16>(w[2 * q] & 0xFFFFu, sv.x), fold_odd<kBF16>(w[2 * q] >> 16, sv.y));
+        w[2 * q + 1] =
+            pack_rn<kBF16>(fold_odd<kBF16>(w[2 * q + 1] & 0xFFFFu, sv.z), fold_odd<kBF16>(w[2 * q + 1] >> 16, sv.w));
       }
     }
     // min / max with NaN propagation; a NaN or ±Inf in the group then shows in mn or mx,
