@@ -7,15 +7,16 @@
 //
 // Layout: a CTA of 256 threads owns 32 consecutive output channels (rows n) and
 // kSlotsPerCta consecutive 128-k slots; 8 lanes share one (row, slot): lane `sub` holds
-// elements [16*sub, 16*sub+16) of the slot (two 16-byte loads, all issued before any
+// elements [16*sub, 16*sub+16) of the slot (one 32-byte load, all issued before any
 // arithmetic).  A group ("different group sizes": GS = 128, 64 or 32) is
 // GS/16 consecutive lanes; min/max are reduced with half2 min/max + log2(GS/16)
-// xor-shuffles.
+// xor-shuffles.  Δ, Z and the scale / zero stores then run once per group on one owner
+// lane (not on every lane of every slot), and the codes fetch Δ and Z from it.
 //
 // Exactness:
-//  * fold: fp32 multiply rounded toward zero + FMA residual gives the product
-//    rounded-to-odd in fp32 (24 bits >= 11 + 2), so the final RN to fp16/bf16 is the
-//    correctly rounded exact product (one rounding, reading S13).
+//  * fold: the odd one of the fp32 products rounded down and up (equal when exact) is the
+//    product rounded-to-odd in fp32 (24 bits >= 11 + 2), so the final RN to fp16/bf16 is
+//    the correctly rounded exact product (one rounding, reading S13).
 //  * r = hi - lo in fp64 (exact for fp16 inputs), Δ = RZ16(r/15) via fp64 division
 //    then RZ->fp32->RZ->fp16 (RZ∘RZ = RZ).
 //  * codes (fp16 path): a non-tie v/Δ is >= 2^-12 from any half-integer (fp16 v, Δ), so
@@ -44,6 +45,7 @@ template <>
 struct Fmt<false> {
   static constexpr uint32_t kExpMask = 0x7C00u;
   __device__ static float to_f(uint16_t b) { return __half2float(__ushort_as_half(b)); }
+  __device__ static float2 to_f2(uint32_t b) { return __half22float2(*reinterpret_cast<const __half2*>(&b)); }
   __device__ static uint16_t from_f_rn(float f) { return __half_as_ushort(__float2half_rn(f)); }
   // NaN-propagating: a NaN anywhere in the group reaches the reduced min and max
   __device__ static uint32_t min2(uint32_t a, uint32_t b) {
@@ -59,6 +61,7 @@ template <>
 struct Fmt<true> {
   static constexpr uint32_t kExpMask = 0x7F80u;
   __device__ static float to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+  __device__ static float2 to_f2(uint32_t b) { return make_float2(__uint_as_float(b << 16), __uint_as_float(b & 0xFFFF0000u)); }
   __device__ static uint16_t from_f_rn(float f) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
   }
@@ -74,15 +77,40 @@ struct Fmt<true> {
   }
 };
 
-// w * s rounded to odd in fp32 (RZ product, sticky bit from the exact FMA residual): its
-// RN to fp16/bf16 is the single rounding RN_fmt(w * s) (24 >= 11 + 2 bits)
-template <bool kBF16>
-__device__ __forceinline__ float fold_odd(uint16_t wbits, float s) {
-  const float w = Fmt<kBF16>::to_f(wbits);
-  float p = __fmul_rz(w, s);
-  const float e = __fmaf_rn(w, s, -p);
-  if (e != 0.0f) p = __uint_as_float(__float_as_uint(p) | 1u);
-  return p;
+// 32-byte loads (LDG.256): a lane's 16 weights / 8 scales in one coalesced instruction
+__device__ __forceinline__ void ld_nc_v8(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_v8f(const float* p, float (&r)[8]) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+      : "l"(p));
+}
+// odd one of two adjacent (or equal) fp32 bit patterns: the low bit of RU, sign-extended
+// (SGXT), selects RU or RD in one LOP3
+__device__ __forceinline__ float odd_of(uint32_t ru, uint32_t rd) {
+  int m;
+  asm("bfe.s32 %0, %1, 0, 1;" : "=r"(m) : "r"(ru));
+  return __uint_as_float((ru & (uint32_t)m) | (rd & ~(uint32_t)m));
+}
+// w * s rounded to odd in fp32 for an element pair: the products rounded down and up
+// (FMUL2.RM / FMUL2.RP) are equal when w * s is exact and adjacent otherwise, and the odd
+// one of two adjacent values is the round-to-odd result; its RN to fp16/bf16 is the single
+// rounding RN_fmt(w * s) (24 >= 11 + 2 bits)
+__device__ __forceinline__ void fold_odd2(float2 w, float s0, float s1, float& p0, float& p1) {
+  uint64_t u, d;
+  asm("{.reg .b64 w, s;\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 s, {%4, %5};\n\t"
+      "mul.rp.f32x2 %0, w, s;\n\t"
+      "mul.rm.f32x2 %1, w, s;}"
+      : "=l"(u), "=l"(d)
+      : "f"(w.x), "f"(w.y), "f"(s0), "f"(s1));
+  p0 = odd_of((uint32_t)u, (uint32_t)d);
+  p1 = odd_of((uint32_t)(u >> 32), (uint32_t)(d >> 32));
 }
 // two round-to-odd products -> RN pair in one packing conversion (F2FP)
 template <bool kBF16>
@@ -94,6 +122,28 @@ __device__ __forceinline__ uint32_t pack_rn(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// fp16 codes of an element pair (see the kernel): RN(v * inv' + 1.5 * 2^23 + Z) for both
+// halves in one FFMA2, the low 16 bits of each are Z + c; gathered as s16x2 and clamped to
+// [0, 15] by one VIMNMX.RELU
+__device__ __forceinline__ uint32_t codes2(uint32_t h2, float inv, float cz) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h2));
+  uint64_t r;
+  asm("{.reg .b64 v, a, c;\n\t"
+      "mov.b64 v, {%1, %2};\n\t"
+      "mov.b64 a, {%3, %3};\n\t"
+      "mov.b64 c, {%4, %4};\n\t"
+      "fma.rn.f32x2 %0, v, a, c;}"
+      : "=l"(r)
+      : "f"(f.x), "f"(f.y), "f"(inv), "f"(cz));
+  return __vimin_s16x2_relu(__byte_perm((uint32_t)r, (uint32_t)(r >> 32), 0x5410), 0x000F000Fu);
+}
+// eight nibbles (low nibble = even k) from four clamped code pairs c[q] = (e_2q, e_2q+1):
+// t = c0 + (c1 << 8) holds e0 | e2 << 8 | e1 << 16 | e3 << 24, and t | t >> 12 has
+// e0 | e1 << 4 | e2 << 8 | e3 << 12 in its low 16 bits
+__device__ __forceinline__ uint32_t nibbles8(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  const uint32_t t0 = c0 + (c1 << 8), t1 = c2 + (c3 << 8);
+  return __byte_perm(t0 | (t0 >> 12), t1 | (t1 >> 12), 0x5410);
+}
 
 template <bool kBF16, int GS>
 __global__ void __launch_bounds__(kThreads)
@@ -101,58 +151,81 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
                 uint8_t* __restrict__ Wq, uint16_t* __restrict__ scales,
                 void* __restrict__ zeros, int zeros_u4, int* __restrict__ nonfinite) {
   constexpr int kLanesPerGroup = GS / 16;
+  // the per-group work (Δ, Z, the scale / zero stores) runs once per group on one owner
+  // lane: in round r lane `sub` owns group sub / kLanesPerGroup of slot
+  // r * kLanesPerGroup + sub % kLanesPerGroup, a lane of that very group (it already holds
+  // the group's reduced min / max); the codes then fetch Δ and Z from the owner
+  constexpr int kRounds = (kSlotsPerCta + kLanesPerGroup - 1) / kLanesPerGroup;
   const int sub = threadIdx.x % kLanesPerSlot;
+  const int lane = threadIdx.x % 32;
   const int n = blockIdx.y * kRowsPerCta + threadIdx.x / kLanesPerSlot;
   const int g0 = blockIdx.x * kSlotsPerCta;  // first slot of the CTA
   const bool row_ok = n < N;
 
   // issue every load of the CTA's groups first (memory-level parallelism)
-  uint4 va[kSlotsPerCta], vb[kSlotsPerCta];
+  uint32_t w[kSlotsPerCta][8];
 #pragma unroll
   for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
     if (row_ok && g < NSL) {
-      const uint16_t* p = W + (size_t)n * K + (size_t)g * kSlot + sub * 16;
-      va[j] = ld_nc_v4(p);
-      vb[j] = ld_nc_v4(p + 8);
+      ld_nc_v8(W + (size_t)n * K + (size_t)g * kSlot + sub * 16, w[j]);
     } else {
-      va[j] = make_uint4(0, 0, 0, 0);
-      vb[j] = va[j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[j][i] = 0u;
     }
   }
 
+  // fold (a3) and the group min / max of every slot
+  uint32_t mn[kSlotsPerCta], mx[kSlotsPerCta];
 #pragma unroll
   for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
-    if (g >= NSL) break;  // uniform across the CTA
-    uint32_t w[8] = {va[j].x, va[j].y, va[j].z, va[j].w, vb[j].x, vb[j].y, vb[j].z, vb[j].w};
-    if (s != nullptr) {
-      const float4* sp = reinterpret_cast<const float4*>(s + (size_t)g * kSlot + sub * 16);
+    if (s != nullptr && g < NSL) {
+      const float* sp = s + (size_t)g * kSlot + sub * 16;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 sv = __ldg(sp + q);
-        w[2 * q] = pack_rn<kBF16>(fold_odd<kBF16>(w[2 * q] & 0xFFFFu, sv.x), fold_odd<kBF16>(w[2 * q] >> 16, sv.y));
-        w[2 * q + 1] =
-            pack_rn<kBF16>(fold_odd<kBF16>(w[2 * q + 1] & 0xFFFFu, sv.z), fold_odd<kBF16>(w[2 * q + 1] >> 16, sv.w));
+      for (int h = 0; h < 2; ++h) {
+        float sv[8];
+        ld_v8f(sp + 8 * h, sv);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float p0, p1;
+          fold_odd2(Fmt<kBF16>::to_f2(w[j][4 * h + q]), sv[2 * q], sv[2 * q + 1], p0, p1);
+          w[j][4 * h + q] = pack_rn<kBF16>(p0, p1);
+        }
       }
     }
     // min / max with NaN propagation; a NaN or ±Inf in the group then shows in mn or mx,
     // so the non-finite test (abs bits >= exponent mask) runs once per group on them
-    uint32_t mn = w[0], mx = w[0];
+    mn[j] = w[j][0], mx[j] = w[j][0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) {
-      mn = Fmt<kBF16>::min2(mn, w[i]);
-      mx = Fmt<kBF16>::max2(mx, w[i]);
+      mn[j] = Fmt<kBF16>::min2(mn[j], w[j][i]);
+      mx[j] = Fmt<kBF16>::max2(mx[j], w[j][i]);
     }
 #pragma unroll
     for (int o = 1; o < kLanesPerGroup; o <<= 1) {
-      mn = Fmt<kBF16>::min2(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = Fmt<kBF16>::max2(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn[j] = Fmt<kBF16>::min2(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
+      mx[j] = Fmt<kBF16>::max2(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
     }
-    const uint32_t amax = __vmaxu2(mn & 0x7FFF7FFFu, mx & 0x7FFF7FFFu);
+  }
+
+  // per group: Δ, Z and their stores, on the owner lane
+  float gv[kRounds];  // fp16: inv' (see the codes); bf16: Δ
+  float gz[kRounds];  // fp16: 1.5 * 2^23 + Z; bf16: Z; -1 marks a non-finite group
+#pragma unroll
+  for (int rd = 0; rd < kRounds; ++rd) {
+    const int j = rd * kLanesPerGroup + sub % kLanesPerGroup;
+    uint32_t gmn = mn[0], gmx = mx[0];
+#pragma unroll
+    for (int jj = 1; jj < kSlotsPerCta; ++jj)
+      if (jj == j) gmn = mn[jj], gmx = mx[jj];
+    const int g = g0 + j;
+    const bool live = j < kSlotsPerCta && g < NSL;
+
+    const uint32_t amax = __vmaxu2(gmn & 0x7FFF7FFFu, gmx & 0x7FFF7FFFu);
     bool nf = ((amax & 0xFFFFu) >= Fmt<kBF16>::kExpMask) || ((amax >> 16) >= Fmt<kBF16>::kExpMask);
-    const float lo = fminf(Fmt<kBF16>::to_f(mn & 0xFFFFu), Fmt<kBF16>::to_f(mn >> 16));
-    const float hi = fmaxf(Fmt<kBF16>::to_f(mx & 0xFFFFu), Fmt<kBF16>::to_f(mx >> 16));
+    const float lo = fminf(Fmt<kBF16>::to_f(gmn & 0xFFFFu), Fmt<kBF16>::to_f(gmn >> 16));
+    const float hi = fmaxf(Fmt<kBF16>::to_f(gmx & 0xFFFFu), Fmt<kBF16>::to_f(gmx >> 16));
 
     // Δ (readings S3, S4)
     const double r = (double)hi - (double)lo;
@@ -178,9 +251,34 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
       z = (float)fmin(fmax(round(-(double)lo / (double)d), 0.0), 15.0);
     }
 
-    // codes for this lane's 16 elements, packed low nibble = even k
+    // packed u4 Z (SQ_ZEROS_U4): rows n and n + 1 of a pair sit 8 lanes apart in the warp
+    // (8 lanes per row) with the same owned group; the even row's lane writes the byte,
+    // low nibble = even n
+    const uint32_t zq = nf ? 0u : (uint32_t)z;
+    const uint32_t zq_odd = __shfl_down_sync(0xffffffffu, zq, kLanesPerSlot);
+    if (row_ok && live) {
+      const size_t gi = (size_t)g * (kSlot / GS) + sub / kLanesPerGroup;
+      scales[gi * N + n] = nf ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(d));
+      if (!zeros_u4)
+        reinterpret_cast<uint16_t*>(zeros)[gi * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
+      else if ((n & 1) == 0)
+        reinterpret_cast<uint8_t*>(zeros)[gi * (N / 2) + n / 2] = (uint8_t)(zq | (zq_odd << 4));
+      if (nf && nonfinite != nullptr) atomicAdd(nonfinite, 1);
+    }
+    gv[rd] = kBF16 ? d : inv;
+    gz[rd] = nf ? -1.0f : (kBF16 ? z : 12582912.0f + z);
+  }
+
+  // codes (a4) of every slot, packed low nibble = even k
+  uint8_t* const wq_row = Wq + (size_t)n * (K / 2) + (size_t)g0 * (kSlot / 2) + sub * 8;
+#pragma unroll
+  for (int j = 0; j < kSlotsPerCta; ++j) {
+    if (g0 + j >= NSL) break;  // uniform across the CTA
+    const int owner = (lane & ~(kLanesPerGroup - 1)) + j % kLanesPerGroup;
+    const float gvj = __shfl_sync(0xffffffffu, gv[j / kLanesPerGroup], owner);
+    const float gzj = __shfl_sync(0xffffffffu, gz[j / kLanesPerGroup], owner);
     uint32_t packed[2] = {0u, 0u};
-    if (!nf) {
+    if (gzj >= 0.0f) {
       if (!kBF16) {
         // RHA(v / Δ) as ONE FFMA per element: RN(v * inv' + 1.5 * 2^23) - 1.5 * 2^23 with
         // inv' = RN(RN(1/Δ) (1 + 2^-17)).  v * inv' = x (1 + 2^-17)(1 + δ), |δ| <= 3 * 2^-24,
@@ -193,51 +291,23 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
         // The magic constant carries + Z: RN(v * inv' + 1.5 * 2^23 + Z) is 1.5 * 2^23 + Z + c
         // (no exact ties remain, see above), whose float bits are 0x4B400000 + (Z + c), so the
         // low 16 bits ARE the signed code Z + c (|Z + c| < 2^15): no subtraction needed.
-        const float cz = 12582912.0f + z;
-        uint32_t bytes[8];
+        uint32_t cc[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // element pair (2q, 2q + 1) = the two halves of w[q]
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-          const uint32_t b0 = __float_as_uint(__fmaf_rn(f.x, inv, cz));
-          const uint32_t b1 = __float_as_uint(__fmaf_rn(f.y, inv, cz));
-          uint32_t cc = __byte_perm(b0, b1, 0x5410);  // (Z + c0, Z + c1) as s16x2
-          asm("max.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0u));
-          asm("min.s16x2 %0, %0, %1;" : "+r"(cc) : "r"(0x000F000Fu));
-          bytes[q] = (cc | (cc >> 12)) & 0xFFu;  // low nibble = even k
-        }
-        // gather the eight bytes: two PRMTs per pair of bytes, one per word
-        packed[0] = __byte_perm(__byte_perm(bytes[0], bytes[1], 0x0040), __byte_perm(bytes[2], bytes[3], 0x0040),
-                                0x5410);
-        packed[1] = __byte_perm(__byte_perm(bytes[4], bytes[5], 0x0040), __byte_perm(bytes[6], bytes[7], 0x0040),
-                                0x5410);
+        for (int q = 0; q < 8; ++q) cc[q] = codes2(w[j][q], gvj, gzj);
+        packed[0] = nibbles8(cc[0], cc[1], cc[2], cc[3]);
+        packed[1] = nibbles8(cc[4], cc[5], cc[6], cc[7]);
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const uint32_t bits = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
+          const uint32_t bits = (i & 1) ? (w[j][i >> 1] >> 16) : (w[j][i >> 1] & 0xFFFFu);
           const float v = Fmt<kBF16>::to_f((uint16_t)bits);
-          float c = (float)round((double)v / (double)d);  // bf16: the gap can be 2^-20, fp64
-          c = fminf(fmaxf(c + z, 0.0f), 15.0f);
+          float c = (float)round((double)v / (double)gvj);  // bf16: the gap can be 2^-20, fp64
+          c = fminf(fmaxf(c + gzj, 0.0f), 15.0f);
           packed[i >> 3] |= (__float_as_uint(c + 8388608.0f) & 0xFu) << (4 * (i & 7));
         }
       }
     }
-    // packed u4 Z (SQ_ZEROS_U4): rows n and n + 1 of a pair sit 8 lanes apart in the warp
-    // (8 lanes per row); the even row's lane writes the byte, low nibble = even n
-    const uint32_t zq = nf ? 0u : (uint32_t)z;
-    const uint32_t zq_odd = __shfl_down_sync(0xffffffffu, zq, kLanesPerSlot);
-    if (row_ok) {
-      *reinterpret_cast<uint2*>(Wq + (size_t)n * (K / 2) + (size_t)g * (kSlot / 2) + sub * 8) =
-          make_uint2(packed[0], packed[1]);
-      if (sub % kLanesPerGroup == 0) {  // first lane of each group
-        const size_t gi = (size_t)g * (kSlot / GS) + sub / kLanesPerGroup;
-        scales[gi * N + n] = nf ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(d));
-        if (!zeros_u4)
-          reinterpret_cast<uint16_t*>(zeros)[gi * N + n] = nf ? (uint16_t)0u : __half_as_ushort(__float2half_rn(z));
-        else if ((n & 1) == 0)
-          reinterpret_cast<uint8_t*>(zeros)[gi * (N / 2) + n / 2] = (uint8_t)(zq | (zq_odd << 4));
-        if (nf && nonfinite != nullptr) atomicAdd(nonfinite, 1);
-      }
-    }
+    if (row_ok) *reinterpret_cast<uint2*>(wq_row + j * (kSlot / 2)) = make_uint2(packed[0], packed[1]);
   }
 }
 
