@@ -37,7 +37,10 @@ constexpr int kThreads = 256;
 constexpr int kRowsPerCta = 32;
 constexpr int kLanesPerSlot = 8;
 constexpr int kSlot = 128;      // k per slot; K % 128 == 0 for every group size
-constexpr int kSlotsPerCta = 4;
+#ifndef SQ_QSLOTS
+#define SQ_QSLOTS 4
+#endif
+constexpr int kSlotsPerCta = SQ_QSLOTS;
 
 template <bool kBF16>
 struct Fmt;
@@ -77,17 +80,12 @@ struct Fmt<true> {
   }
 };
 
-// 32-byte loads (LDG.256): a lane's 16 weights / 8 scales in one coalesced instruction
+// 32-byte load (LDG.256): a lane's 16 weights of a slot in one coalesced instruction
 __device__ __forceinline__ void ld_nc_v8(const void* p, uint32_t (&r)[8]) {
   asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                  "=r"(r[7])
                : "l"(p));
-}
-__device__ __forceinline__ void ld_v8f(const float* p, float (&r)[8]) {
-  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
-      : "l"(p));
 }
 // odd one of two adjacent (or equal) fp32 bit patterns: the low bit of RU, sign-extended
 // (SGXT), selects RU or RD in one LOP3
@@ -146,7 +144,10 @@ __device__ __forceinline__ uint32_t nibbles8(uint32_t c0, uint32_t c1, uint32_t 
 }
 
 template <bool kBF16, int GS>
-__global__ void __launch_bounds__(kThreads)
+#ifndef SQ_QMINB
+#define SQ_QMINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, SQ_QMINB)
 quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int N, int K, int NSL,
                 uint8_t* __restrict__ Wq, uint16_t* __restrict__ scales,
                 void* __restrict__ zeros, int zeros_u4, int* __restrict__ nonfinite) {
@@ -175,23 +176,35 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
     }
   }
 
+  // the CTA's s (shared by its 32 rows) staged in shared memory while the weight loads fly,
+  // permuted so that float4 q of lane `sub` sits at (q * 8 + sub): one conflict-free
+  // wavefront per LDS.128 (the s loads of a slot otherwise wait a full L2 latency)
+  __shared__ __align__(16) float4 s_sm[kSlotsPerCta * kSlot / 4];
+  if (s != nullptr) {  // uniform
+#pragma unroll
+    for (int i = threadIdx.x; i < kSlotsPerCta * kSlot / 4; i += kThreads) {
+      const int j = i / (kSlot / 4), e = i % (kSlot / 4);  // float4 e of slot j = (sub e/4, q e%4)
+      s_sm[j * (kSlot / 4) + (e % 4) * 8 + e / 4] =
+          g0 + j < NSL ? __ldg(reinterpret_cast<const float4*>(s + (size_t)(g0 + j) * kSlot) + e)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+  }
+
   // fold (a3) and the group min / max of every slot
   uint32_t mn[kSlotsPerCta], mx[kSlotsPerCta];
 #pragma unroll
   for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
     if (s != nullptr && g < NSL) {
-      const float* sp = s + (size_t)g * kSlot + sub * 16;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float sv[8];
-        ld_v8f(sp + 8 * h, sv);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float p0, p1;
-          fold_odd2(Fmt<kBF16>::to_f2(w[j][4 * h + q]), sv[2 * q], sv[2 * q + 1], p0, p1);
-          w[j][4 * h + q] = pack_rn<kBF16>(p0, p1);
-        }
+      for (int q = 0; q < 4; ++q) {
+        const float4 sv = s_sm[j * (kSlot / 4) + q * 8 + sub];
+        float p0, p1, p2, p3;
+        fold_odd2(Fmt<kBF16>::to_f2(w[j][2 * q]), sv.x, sv.y, p0, p1);
+        fold_odd2(Fmt<kBF16>::to_f2(w[j][2 * q + 1]), sv.z, sv.w, p2, p3);
+        w[j][2 * q] = pack_rn<kBF16>(p0, p1);
+        w[j][2 * q + 1] = pack_rn<kBF16>(p2, p3);
       }
     }
     // min / max with NaN propagation; a NaN or ±Inf in the group then shows in mn or mx,
