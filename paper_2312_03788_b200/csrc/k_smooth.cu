@@ -5,8 +5,8 @@
 //   a2  s[k] = max(a,eps)^alpha / max(w,eps)^(1-alpha), fp64, RN to fp32
 //
 // HBM-bound column reduction: each thread owns 8 consecutive columns (one 16-byte
-// vector per row), a CTA covers 2048 columns x a slice of rows, and the per-column
-// maxima are merged with atomicMax on the fp32 bit pattern (all values >= 0, so
+// vector per row) of every kRowLanes-th row of its CTA's row slice; the row lanes of a
+// warp are merged with shuffles, and the per-column maxima of the CTAs with atomicMax on the fp32 bit pattern (all values >= 0, so
 // the unsigned order of the bits is the numeric order; NaN sorts above Inf and so
 // propagates, like numpy's max).  Inside a thread the maxima are kept as packed
 // 16-bit |x| bit patterns and merged with one SIMD unsigned max per pair
@@ -19,7 +19,15 @@ namespace {
 
 constexpr int kColsPerThread = 8;
 constexpr int kThreads = 256;
-constexpr int kColsPerCta = kColsPerThread * kThreads;
+// A warp = kRL row lanes x (32 / kRL) column threads: each row lane walks every kRL-th
+// row of the CTA's slice, the lanes are merged with warp shuffles, and then one atomicMax
+// per column leaves the CTA.  kRL = 1 (a warp reads 512 contiguous bytes of a row, a CTA
+// 4 KB) suits slices of >= 128 rows per CTA; below that the atomics, not the loads, bound
+// it and kRL = 8 (8x fewer atomics per byte) wins (profiles/r02/colabsmax_rowlanes_ab.jsonl)
+constexpr int kRowsInFlight = 4;  // rows per thread and loop iteration
+constexpr int kCtasPerSm = 4;     // grid target (row slices x column blocks)
+template <int kRL>
+constexpr int cols_per_cta() { return kColsPerThread * (32 / kRL) * (kThreads / 32); }
 
 __device__ __forceinline__ uint32_t vmaxu2(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
 
@@ -29,36 +37,53 @@ __device__ __forceinline__ uint32_t abs16_to_f32bits(uint32_t h) {
   return __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(h))));
 }
 
-template <bool kBF16>
+template <bool kBF16, int kRowLanes>
 __global__ void __launch_bounds__(kThreads)
 colabsmax_kernel(const uint16_t* __restrict__ X, int64_t rows, int64_t K, int64_t rows_per_cta,
                  unsigned* __restrict__ out) {
-  const int64_t col0 = (int64_t)blockIdx.x * kColsPerCta + (int64_t)threadIdx.x * kColsPerThread;
-  if (col0 >= K) return;
+  constexpr int kColThreads = 32 / kRowLanes;  // per warp
+  constexpr int kColsPerCta = cols_per_cta<kRowLanes>();
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int rl = lane / kColThreads;  // row lane
+  const int64_t col0 = (int64_t)blockIdx.x * kColsPerCta +
+                       (int64_t)(warp * kColThreads + lane % kColThreads) * kColsPerThread;
+  const bool col_ok = col0 < K;  // K % 8 == 0: a thread's 8 columns are all valid or none
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
   const int64_t r1 = min(rows, r0 + rows_per_cta);
   uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-  const uint16_t* p = X + r0 * K + col0;
-  int64_t r = r0;
-  // 4 rows in flight per iteration
-  for (; r + 4 <= r1; r += 4, p += 4 * K) {
-    uint4 v0 = ld_nc_v4(p), v1 = ld_nc_v4(p + K), v2 = ld_nc_v4(p + 2 * K), v3 = ld_nc_v4(p + 3 * K);
-    m0 = vmaxu2(m0, vmaxu2(vmaxu2(v0.x & 0x7FFF7FFFu, v1.x & 0x7FFF7FFFu),
-                           vmaxu2(v2.x & 0x7FFF7FFFu, v3.x & 0x7FFF7FFFu)));
-    m1 = vmaxu2(m1, vmaxu2(vmaxu2(v0.y & 0x7FFF7FFFu, v1.y & 0x7FFF7FFFu),
-                           vmaxu2(v2.y & 0x7FFF7FFFu, v3.y & 0x7FFF7FFFu)));
-    m2 = vmaxu2(m2, vmaxu2(vmaxu2(v0.z & 0x7FFF7FFFu, v1.z & 0x7FFF7FFFu),
-                           vmaxu2(v2.z & 0x7FFF7FFFu, v3.z & 0x7FFF7FFFu)));
-    m3 = vmaxu2(m3, vmaxu2(vmaxu2(v0.w & 0x7FFF7FFFu, v1.w & 0x7FFF7FFFu),
-                           vmaxu2(v2.w & 0x7FFF7FFFu, v3.w & 0x7FFF7FFFu)));
+  if (col_ok) {
+    const uint16_t* p = X + (r0 + rl) * K + col0;
+    int64_t r = r0 + rl;
+    // kRowsInFlight of this lane's rows per iteration, every load issued before any max
+    for (; r + (kRowsInFlight - 1) * kRowLanes < r1; r += kRowsInFlight * kRowLanes, p += kRowsInFlight * kRowLanes * K) {
+      uint4 v[kRowsInFlight];
+#pragma unroll
+      for (int i = 0; i < kRowsInFlight; ++i) v[i] = ld_nc_v4(p + (int64_t)i * kRowLanes * K);
+#pragma unroll
+      for (int i = 0; i < kRowsInFlight; ++i) {
+        m0 = vmaxu2(m0, v[i].x & 0x7FFF7FFFu);
+        m1 = vmaxu2(m1, v[i].y & 0x7FFF7FFFu);
+        m2 = vmaxu2(m2, v[i].z & 0x7FFF7FFFu);
+        m3 = vmaxu2(m3, v[i].w & 0x7FFF7FFFu);
+      }
+    }
+    for (; r < r1; r += kRowLanes, p += kRowLanes * K) {
+      uint4 v = ld_nc_v4(p);
+      m0 = vmaxu2(m0, v.x & 0x7FFF7FFFu);
+      m1 = vmaxu2(m1, v.y & 0x7FFF7FFFu);
+      m2 = vmaxu2(m2, v.z & 0x7FFF7FFFu);
+      m3 = vmaxu2(m3, v.w & 0x7FFF7FFFu);
+    }
   }
-  for (; r < r1; ++r, p += K) {
-    uint4 v = ld_nc_v4(p);
-    m0 = vmaxu2(m0, v.x & 0x7FFF7FFFu);
-    m1 = vmaxu2(m1, v.y & 0x7FFF7FFFu);
-    m2 = vmaxu2(m2, v.z & 0x7FFF7FFFu);
-    m3 = vmaxu2(m3, v.w & 0x7FFF7FFFu);
+  // merge the row lanes (same columns, lanes kColThreads apart)
+#pragma unroll
+  for (int o = kColThreads; o < 32; o <<= 1) {
+    m0 = vmaxu2(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    m1 = vmaxu2(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    m2 = vmaxu2(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    m3 = vmaxu2(m3, __shfl_xor_sync(0xffffffffu, m3, o));
   }
+  if (!col_ok || rl != 0) return;
   const uint32_t m[4] = {m0, m1, m2, m3};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -90,22 +115,33 @@ __global__ void smooth_finalize_kernel(const float* __restrict__ act_max, float*
 
 }  // namespace
 
-cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K, float* out,
-                             cudaStream_t st) {
-  const int64_t kblocks = (K + kColsPerCta - 1) / kColsPerCta;
-  const int64_t target = 4ll * num_sms();
+template <int kRL>
+static cudaError_t launch_colabsmax_rl(const void* X, int dtype, int64_t rows, int64_t K, float* out,
+                                       cudaStream_t st) {
+  const int64_t kblocks = (K + cols_per_cta<kRL>() - 1) / cols_per_cta<kRL>();
+  const int64_t target = (int64_t)kCtasPerSm * num_sms();
   int64_t rsplit = (target + kblocks - 1) / kblocks;
   rsplit = std::max<int64_t>(1, std::min<int64_t>(rsplit, (rows + 15) / 16));
   const int64_t rows_per_cta = (rows + rsplit - 1) / rsplit;
   rsplit = (rows + rows_per_cta - 1) / rows_per_cta;
   dim3 grid((unsigned)kblocks, (unsigned)rsplit);
   if (dtype == SQ_BF16)
-    colabsmax_kernel<true><<<grid, kThreads, 0, st>>>((const uint16_t*)X, rows, K, rows_per_cta,
-                                                      (unsigned*)out);
+    colabsmax_kernel<true, kRL><<<grid, kThreads, 0, st>>>((const uint16_t*)X, rows, K, rows_per_cta,
+                                                           (unsigned*)out);
   else
-    colabsmax_kernel<false><<<grid, kThreads, 0, st>>>((const uint16_t*)X, rows, K, rows_per_cta,
-                                                       (unsigned*)out);
+    colabsmax_kernel<false, kRL><<<grid, kThreads, 0, st>>>((const uint16_t*)X, rows, K, rows_per_cta,
+                                                            (unsigned*)out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K, float* out,
+                             cudaStream_t st) {
+  // rows per CTA of the one-row-lane grid: below 128 its atomics dominate
+  const int64_t kblocks1 = (K + cols_per_cta<1>() - 1) / cols_per_cta<1>();
+  const int64_t slices1 = std::max<int64_t>(
+      1, std::min<int64_t>(((int64_t)kCtasPerSm * num_sms() + kblocks1 - 1) / kblocks1, (rows + 15) / 16));
+  if ((rows + slices1 - 1) / slices1 >= 128) return launch_colabsmax_rl<1>(X, dtype, rows, K, out, st);
+  return launch_colabsmax_rl<8>(X, dtype, rows, K, out, st);
 }
 
 cudaError_t launch_smooth_finalize(const float* act_max, float* s, int64_t K, double alpha,
