@@ -37,10 +37,8 @@ constexpr int kThreads = 256;
 constexpr int kRowsPerCta = 32;
 constexpr int kLanesPerSlot = 8;
 constexpr int kSlot = 128;      // k per slot; K % 128 == 0 for every group size
-#ifndef SQ_QSLOTS
-#define SQ_QSLOTS 4
-#endif
-constexpr int kSlotsPerCta = SQ_QSLOTS;
+constexpr int kSlotsPerCta = 4;  // 2 and 8 lose (profiles/r02/quantize_occupancy_ab.jsonl)
+constexpr int kMinCtasPerSm = 4; // 64 registers: four CTAs per SM beat 2, 3 and 5
 
 template <bool kBF16>
 struct Fmt;
@@ -144,10 +142,7 @@ __device__ __forceinline__ uint32_t nibbles8(uint32_t c0, uint32_t c1, uint32_t 
 }
 
 template <bool kBF16, int GS>
-#ifndef SQ_QMINB
-#define SQ_QMINB 4
-#endif
-__global__ void __launch_bounds__(kThreads, SQ_QMINB)
+__global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int N, int K, int NSL,
                 uint8_t* __restrict__ Wq, uint16_t* __restrict__ scales,
                 void* __restrict__ zeros, int zeros_u4, int* __restrict__ nonfinite) {
