@@ -108,6 +108,25 @@ __device__ __forceinline__ void fold_odd2(float2 w, float s0, float s1, float& p
   p0 = odd_of((uint32_t)u, (uint32_t)d);
   p1 = odd_of((uint32_t)(u >> 32), (uint32_t)(d >> 32));
 }
+// fp16 pair, s >= 0 (sign bits clear): the product's magnitude |w| * s is formed from |w|
+// (the abs is a free operand modifier of the conversion), so its RZ value is RD, RU is RD
+// or RD + 1, and the round-to-odd value is RD | (RU & 1) — one LOP3; RN to fp16 commutes
+// with the sign, which is w's and is ORed back into the packed pair
+__device__ __forceinline__ uint32_t fold_pos2(uint32_t h, float s0, float s1) {
+  const __half2 a2 = __habs2(*reinterpret_cast<const __half2*>(&h));
+  const float2 a = __half22float2(a2);
+  uint64_t u, d;
+  asm("{.reg .b64 w, s;\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 s, {%4, %5};\n\t"
+      "mul.rp.f32x2 %0, w, s;\n\t"
+      "mul.rm.f32x2 %1, w, s;}"
+      : "=l"(u), "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(s0), "f"(s1));
+  const uint32_t ru0 = (uint32_t)u, rd0 = (uint32_t)d, ru1 = (uint32_t)(u >> 32), rd1 = (uint32_t)(d >> 32);
+  const __half2 r = __floats2half2_rn(__uint_as_float(rd0 | (ru0 & 1u)), __uint_as_float(rd1 | (ru1 & 1u)));
+  return *reinterpret_cast<const uint32_t*>(&r) | (h & 0x80008000u);
+}
 // two round-to-odd products -> RN pair in one packing conversion (F2FP)
 template <bool kBF16>
 __device__ __forceinline__ uint32_t pack_rn(float lo, float hi) {
@@ -134,11 +153,18 @@ __device__ __forceinline__ uint32_t codes2(uint32_t h2, float inv, float cz) {
   return __vimin_s16x2_relu(__byte_perm((uint32_t)r, (uint32_t)(r >> 32), 0x5410), 0x000F000Fu);
 }
 // eight nibbles (low nibble = even k) from four clamped code pairs c[q] = (e_2q, e_2q+1):
-// t = c0 + (c1 << 8) holds e0 | e2 << 8 | e1 << 16 | e3 << 24, and t | t >> 12 has
+// t = c0 + (c1 << 8) holds e0 | e2 << 8 | e1 << 16 | e3 << 24, and t + (t >> 12) has
 // e0 | e1 << 4 | e2 << 8 | e3 << 12 in its low 16 bits
+// (the bit fields of t and t >> 12 are disjoint, so | is +; both steps are integer
+// multiply-adds, which issue on the FMA pipe and leave the ALU pipe, the bound, to the rest)
+__device__ __forceinline__ uint32_t nib4(uint32_t ca, uint32_t cb) {
+  uint32_t t, u;
+  asm("mad.lo.u32 %0, %1, 256, %2;" : "=r"(t) : "r"(cb), "r"(ca));
+  asm("mad.hi.u32 %0, %1, 1048576, %1;" : "=r"(u) : "r"(t));
+  return u;
+}
 __device__ __forceinline__ uint32_t nibbles8(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
-  const uint32_t t0 = c0 + (c1 << 8), t1 = c2 + (c3 << 8);
-  return __byte_perm(t0 | (t0 >> 12), t1 | (t1 >> 12), 0x5410);
+  return __byte_perm(nib4(c0, c1), nib4(c2, c3), 0x5410);
 }
 
 template <bool kBF16, int GS>
@@ -175,15 +201,18 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
   // permuted so that float4 q of lane `sub` sits at (q * 8 + sub): one conflict-free
   // wavefront per LDS.128 (the s loads of a slot otherwise wait a full L2 latency)
   __shared__ __align__(16) float4 s_sm[kSlotsPerCta * kSlot / 4];
+  bool s_pos = false;  // every staged s has a clear sign bit (CTA-uniform)
   if (s != nullptr) {  // uniform
+    uint32_t sign = 0u;
 #pragma unroll
     for (int i = threadIdx.x; i < kSlotsPerCta * kSlot / 4; i += kThreads) {
       const int j = i / (kSlot / 4), e = i % (kSlot / 4);  // float4 e of slot j = (sub e/4, q e%4)
-      s_sm[j * (kSlot / 4) + (e % 4) * 8 + e / 4] =
-          g0 + j < NSL ? __ldg(reinterpret_cast<const float4*>(s + (size_t)(g0 + j) * kSlot) + e)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = g0 + j < NSL ? __ldg(reinterpret_cast<const float4*>(s + (size_t)(g0 + j) * kSlot) + e)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      sign |= __float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) | __float_as_uint(v.w);
+      s_sm[j * (kSlot / 4) + (e % 4) * 8 + e / 4] = v;
     }
-    __syncthreads();
+    s_pos = !__syncthreads_or((int)(sign >> 31));
   }
 
   // fold (a3) and the group min / max of every slot
@@ -191,7 +220,14 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
 #pragma unroll
   for (int j = 0; j < kSlotsPerCta; ++j) {
     const int g = g0 + j;
-    if (s != nullptr && g < NSL) {
+    if (!kBF16 && s_pos && g < NSL) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 sv = s_sm[j * (kSlot / 4) + q * 8 + sub];
+        w[j][2 * q] = fold_pos2(w[j][2 * q], sv.x, sv.y);
+        w[j][2 * q + 1] = fold_pos2(w[j][2 * q + 1], sv.z, sv.w);
+      }
+    } else if (s != nullptr && g < NSL) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float4 sv = s_sm[j * (kSlot / 4) + q * 8 + sub];

@@ -126,6 +126,26 @@ def test_quantize_edge_groups_bitexact():
     _check_quant(W, s, q2, nonfinite=nf)
 
 
+def test_quantize_fold_ties_and_signs_bitexact():
+    """Eq. 5 fold RN(W * s) (reading S13) on products that land exactly on fp16 midpoints or
+    one fp32 ulp beside them, through both kernel paths in one launch: CTAs whose 512-k slice
+    of s has only clear sign bits take the |w|-based fold, the others (a negative s, -0.0)
+    the signed one."""
+    N, K = 64, 4096
+    W = synth.weights(N, K, seed=21, heavy=True)
+    r = synth.rng(22)
+    base = np.array([1 + 2.0 ** -11, 1 - 2.0 ** -12, 1 + 3 * 2.0 ** -12, 0.75 * (1 + 2.0 ** -10),
+                     1 + 2.0 ** -11 + 2.0 ** -23, 1 + 2.0 ** -11 - 2.0 ** -23, 2.0 ** -14, 3.0],
+                    dtype=np.float64)
+    sv = base[r.integers(0, len(base), size=K)] * np.exp2(r.integers(-3, 4, size=K))
+    sv[K // 2:] *= np.where(r.random(K - K // 2) < 0.1, -1.0, 1.0)   # second half: some negative
+    sv[3 * K // 4 + 5] = -0.0
+    s = sv.astype(np.float32)
+    nf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    q = sq.quantize_pack_groupwise(_t(W), _t(s), nonfinite=nf)
+    _check_quant(W, s, q, nonfinite=nf)
+
+
 def test_quantize_nonfinite_groups():
     bad = synth.nonfinite_groups(128)
     W = np.concatenate([bad, synth.weights(5, 128, seed=8)]).astype(np.float16)
