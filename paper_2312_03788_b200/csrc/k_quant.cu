@@ -5,7 +5,7 @@
 //   a4  Δ = RZ16((max - min) / 15), Z, codes   PAPER.md:88-93 Eq. 1; readings S1-S4
 //       pack: low nibble = even k
 //
-// Layout: a CTA of 256 threads owns 32 consecutive output channels (rows n) and
+// Layout: a CTA of 128 threads owns 16 consecutive output channels (rows n) and
 // kSlotsPerCta consecutive 128-k slots; 8 lanes share one (row, slot): lane `sub` holds
 // elements [16*sub, 16*sub+16) of the slot (one 32-byte load, all issued before any
 // arithmetic).  A group ("different group sizes": GS = 128, 64 or 32) is
@@ -33,12 +33,12 @@ namespace sq {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kRowsPerCta = 32;
+constexpr int kThreads = 128;  // 64 and 512 lose (profiles/r02/quantize_cta_size_ab.jsonl)
+constexpr int kRowsPerCta = 16;
 constexpr int kLanesPerSlot = 8;
 constexpr int kSlot = 128;      // k per slot; K % 128 == 0 for every group size
 constexpr int kSlotsPerCta = 4;  // 2 and 8 lose (profiles/r02/quantize_occupancy_ab.jsonl)
-constexpr int kMinCtasPerSm = 4; // 64 registers: four CTAs per SM beat 2, 3 and 5
+constexpr int kMinCtasPerSm = 8; // 64 registers (1024 threads per SM) beat 48, 80 and 128
 
 template <bool kBF16>
 struct Fmt;
@@ -197,7 +197,7 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
     }
   }
 
-  // the CTA's s (shared by its 32 rows) staged in shared memory while the weight loads fly,
+  // the CTA's s (shared by its 16 rows) staged in shared memory while the weight loads fly,
   // permuted so that float4 q of lane `sub` sits at (q * 8 + sub): one conflict-free
   // wavefront per LDS.128 (the s loads of a slot otherwise wait a full L2 latency)
   __shared__ __align__(16) float4 s_sm[kSlotsPerCta * kSlot / 4];
