@@ -24,7 +24,8 @@
 //    magic constant) is RHA(v/Δ): the factor pushes exact ties away from zero by more than
 //    the product's error and moves non-ties by less than the gap (see the code).  The
 //    clamp and the nibble packing then run on two codes per instruction (s16x2).
-//  * codes (bf16 path): the gap can be as small as 2^-20, so v/Δ uses fp64 division.
+//  * codes (bf16 path): the gap can be as small as 2^-20, so the rounding of v/Δ is
+//    decided exactly by the signs of two FMA residuals at the candidate midpoints.
 #include <algorithm>
 
 #include "sq_internal.cuh"
@@ -341,11 +342,23 @@ quantize_kernel(const uint16_t* __restrict__ W, const float* __restrict__ s, int
         packed[0] = nibbles8(cc[0], cc[1], cc[2], cc[3]);
         packed[1] = nibbles8(cc[4], cc[5], cc[6], cc[7]);
       } else {
+        // bf16: a non-tie v / Δ can lie 2^-20 from a half-integer, too close for the one-FFMA
+        // rounding.  c0 = rint(v * RN(1/Δ)) is within 1 of RHA(v / Δ) (|v / Δ| < 2^13 in a
+        // finite group, relative error < 2^-22), and the two candidate midpoints are decided
+        // exactly: fma(-(c0 ± 1/2), Δ, v) is v - (c0 ± 1/2) Δ rounded once, so its sign is
+        // exact and it is 0 only at an exact tie (the exact value is a multiple of 2^-133,
+        // far above fp32's 2^-149 underflow), which RHA sends away from zero
+        const float inv = __frcp_rn(gvj);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const uint32_t bits = (i & 1) ? (w[j][i >> 1] >> 16) : (w[j][i >> 1] & 0xFFFFu);
           const float v = Fmt<kBF16>::to_f((uint16_t)bits);
-          float c = (float)round((double)v / (double)gvj);  // bf16: the gap can be 2^-20, fp64
+          const float c0 = rintf(v * inv);
+          const float th = __fmaf_rn(-(c0 + 0.5f), gvj, v);  // v/Δ - (c0 + 1/2), scaled by Δ
+          const float tl = __fmaf_rn(-(c0 - 0.5f), gvj, v);  // v/Δ - (c0 - 1/2), scaled by Δ
+          float c = c0;
+          if (th > 0.0f || (th == 0.0f && c0 >= 0.0f)) c = c0 + 1.0f;
+          else if (tl < 0.0f || (tl == 0.0f && c0 <= 0.0f)) c = c0 - 1.0f;
           c = fminf(fmaxf(c + gzj, 0.0f), 15.0f);
           packed[i >> 3] |= (__float_as_uint(c + 8388608.0f) & 0xFu) << (4 * (i & 7));
         }

@@ -165,6 +165,35 @@ def test_quantize_bf16_weights_bitexact():
     _check_quant(Wbits, s, q, w_dtype="bf16", nonfinite=nf)
 
 
+
+def test_quantize_bf16_ties_and_near_ties_bitexact():
+    """Eq. 1 codes RHA(v / Δ) (reading S2) for bf16 weights at exact ties and one bf16 ulp
+    beside them: groups with lo = 0, hi = 15/16 (Δ = 1/16, Z = 0), their negatives
+    (Z = 15), scaled by powers of two, and random bf16 groups; RTN and an exact
+    power-of-two fold."""
+    r = synth.rng(31)
+    rows = []
+    for e in range(-12, 13, 3):
+        for sign in (1.0, -1.0):
+            base = np.concatenate([[0.0, 15 / 16], (np.arange(15) + 0.5) / 16, np.arange(16) / 16])
+            g = np.resize(base, 128)
+            near = (np.arange(15) + 0.5) / 16 * (1 + 2.0 ** -7)    # one bf16 ulp above a tie
+            g[40:55] = near
+            g[60:75] = (np.arange(15) + 0.5) / 16 * (1 - 2.0 ** -8)  # one ulp below
+            rows.append(sign * g * 2.0 ** e)
+    rows.append(r.normal(0, 1, size=128) * 2.0 ** -20)
+    rows.append(r.normal(0, 1, size=128) * 1e3)
+    W = np.stack(rows)
+    W = np.concatenate([W, W[:, ::-1]], axis=1)                   # [R][256]
+    pad = (-W.shape[0]) % 8
+    W = np.concatenate([W, np.resize(W[:1], (pad, W.shape[1]))]).astype(np.float32)
+    Wb = torch.from_numpy(W).to(torch.bfloat16)
+    Wbits = Wb.view(torch.int16).numpy().view(np.uint16)
+    for s in (None, np.float32(2.0) ** synth.rng(32).integers(-3, 4, size=256).astype(np.float32)):
+        nf = torch.zeros(1, dtype=torch.int32, device=DEV)
+        q = sq.quantize_pack_groupwise(Wb.to(DEV), None if s is None else _t(s), nonfinite=nf)
+        _check_quant(Wbits, s, q, w_dtype="bf16", nonfinite=nf)
+
 # ------------------------------------------------------------------ a6/a7 GEMM
 class GemmCase:
     """GPU output and the oracle's exact result of one GEMM, plus what the element-wise

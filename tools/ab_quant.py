@@ -1,6 +1,7 @@
 """A/B timing of the quantize kernel (sq_quantize_pack_groupwise, fold + Eq. 1 + pack) from
 several libsq builds in one process: python tools/ab_quant.py lib1.so lib2.so ...
-AB_WHAT=absmax times the column abs-max instead (sq_act_absmax over W[N][K], 2NK bytes)."""
+AB_WHAT=absmax times the column abs-max instead (sq_act_absmax over W[N][K], 2NK bytes);
+AB_DTYPE=bf16 quantizes bf16 weights."""
 import ctypes
 import json
 import os
@@ -23,7 +24,8 @@ def main():
     if os.environ.get("AB_WHAT") == "absmax":
         return absmax(libs, peak, dev)
     for N, K in ((22016, 8192), (8192, 22016), (10240, 8192)):
-        W = (torch.randn(N, K, device=dev) * 0.02).half()
+        bf16 = os.environ.get("AB_DTYPE") == "bf16"
+        W = (torch.randn(N, K, device=dev) * 0.02).to(torch.bfloat16 if bf16 else torch.float16)
         s = (torch.rand(K, device=dev) + 0.5).float()
         Wq = torch.empty(N, K // 2, dtype=torch.uint8, device=dev)
         sc = torch.empty(K // 128, N, dtype=torch.int16, device=dev)
@@ -38,7 +40,7 @@ def main():
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
                     for _ in range(10):
-                        assert L.sq_quantize_pack_groupwise(W.data_ptr(), 0, s.data_ptr() if smooth else None, N, K,
+                        assert L.sq_quantize_pack_groupwise(W.data_ptr(), 1 if bf16 else 0, s.data_ptr() if smooth else None, N, K,
                                                             128, Wq.data_ptr(), sc.data_ptr(), z.data_ptr(), None,
                                                             st) == 0
                     e1.record()
