@@ -136,11 +136,13 @@ static cudaError_t launch_colabsmax_rl(const void* X, int dtype, int64_t rows, i
 
 cudaError_t launch_colabsmax(const void* X, int dtype, int64_t rows, int64_t K, float* out,
                              cudaStream_t st) {
-  // rows per CTA of the one-row-lane grid: below 128 its atomics dominate
+  // rows per CTA of the one-row-lane grid: below 128 its atomics dominate, and below 256
+  // when >= 128 row slices contend for every column (K <= 8192 on this GPU)
   const int64_t kblocks1 = (K + cols_per_cta<1>() - 1) / cols_per_cta<1>();
   const int64_t slices1 = std::max<int64_t>(
       1, std::min<int64_t>(((int64_t)kCtasPerSm * num_sms() + kblocks1 - 1) / kblocks1, (rows + 15) / 16));
-  if ((rows + slices1 - 1) / slices1 >= 128) return launch_colabsmax_rl<1>(X, dtype, rows, K, out, st);
+  if ((rows + slices1 - 1) / slices1 >= (slices1 >= 128 ? 256 : 128))
+    return launch_colabsmax_rl<1>(X, dtype, rows, K, out, st);
   return launch_colabsmax_rl<8>(X, dtype, rows, K, out, st);
 }
 
