@@ -794,8 +794,8 @@ def main():
         quant = {"value": qb_all / tq / 1e9, "unit": "GB/s", "ms_per_layer": tq * 1e3,
                  "frac_hbm": qb_all / tq / 1e9 / (hbm_peak * world),
                  "bound_note": "two passes: w_max column abs-max (HBM-bound) then the exact fold + Eq. 1 "
-                               "quantize (ALU pipe the bound: ncu ALU 73 %, issue 75 %, 14 lane-instructions "
-                               "per weight, profiles/r02/ncu/prof_quant_final.*); algorithmic bytes 2NK (w_max) + 2NK + 4K + NK/2 + 4NK/128 (quantize)",
+                               "quantize (ncu: ALU pipe 71 %, issue 78 %, DRAM 58 %, 13.5 lane-instructions "
+                               "per weight, profiles/r02/ncu/prof_quant_end.*); algorithmic bytes 2NK (w_max) + 2NK + 4K + NK/2 + 4NK/128 (quantize)",
                  "what": "sq_smooth_scales (w_max + Eq. 6) + sq_quantize_pack_groupwise for one layer"}
         del Ws
 
